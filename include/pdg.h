@@ -156,6 +156,10 @@ typedef struct pdg_pattern {
 int pdg_abi_version(void);
 const char* pdg_last_error(void);
 
+/* Number of kernels this library has launched in this process (benchmark
+ * accounting: the driver compares it with the profiler's launch list). */
+int64_t pdg_launch_count(void);
+
 /* Bytes of device scratch needed by pdg_adjacency / pdg_pattern_offsets. */
 size_t pdg_workspace_bytes(int64_t n_elements, int64_t n_interfaces);
 

@@ -83,7 +83,7 @@ class Pattern(C.Structure):
 
 
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
-EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_workspace_bytes", "pdg_adjacency",
+EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes", "pdg_adjacency",
            "pdg_pattern_offsets", "pdg_pattern_fill", "pdg_face_prepass", "pdg_assemble",
            "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks")
 
@@ -102,6 +102,7 @@ def load():
     P = C.POINTER
     lib.pdg_abi_version.restype = C.c_int
     lib.pdg_last_error.restype = C.c_char_p
+    lib.pdg_launch_count.restype = C.c_int64
     lib.pdg_workspace_bytes.restype = C.c_size_t
     lib.pdg_workspace_bytes.argtypes = [_i64, _i64]
     lib.pdg_adjacency.argtypes = [P(Mesh), _p, _p, _p, _p, C.c_size_t, _p]
@@ -117,7 +118,7 @@ def load():
     lib.pdg_element_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params), _p,
                                        _i64, _p, _p, _p, _p]
     for name in EXPORTS:
-        if name not in ("pdg_abi_version", "pdg_last_error", "pdg_workspace_bytes"):
+        if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes"):
             getattr(lib, name).restype = C.c_int
     if lib.pdg_abi_version() != 1:
         raise EngineUnavailable("libpdg.so ABI version mismatch")

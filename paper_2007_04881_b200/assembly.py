@@ -587,6 +587,46 @@ class SipgPlan:
         return out
 
 
+class HostIO:
+    """Pinned-host staging for end-to-end runs of a plan: every ``upload()``
+    copies the mesh arrays host->device (the assembly inputs), every
+    ``download()`` moves the assembled CSR (row_ptr, col_idx, values) and the
+    RHS device->host through a pinned staging ring of ``chunk_bytes``.  The
+    bytes moved are the full result; only the host-side retention is bounded
+    (a 4M-element p=4 matrix is ~100 GB)."""
+
+    def __init__(self, plan: "SipgPlan", chunk_bytes: int = 1 << 30):
+        torch = _torch()
+        self.plan = plan
+        self.inputs = {}
+        for attr, _ in _MESH_FIELDS:
+            src = plan.dm.t[attr]
+            h = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+            h.copy_(src)
+            self.inputs[attr] = h
+        self.h2d_bytes = sum(int(t.numel() * t.element_size()) for t in self.inputs.values())
+        self.stage = torch.empty(chunk_bytes, dtype=torch.uint8, pin_memory=True)
+        outs = (plan.row_ptr, plan.col_idx, plan.values, plan.rhs)
+        self.d2h_bytes = sum(int(t.numel() * t.element_size()) for t in outs)
+
+    def upload(self):
+        torch = _torch()
+        with torch.cuda.stream(self.plan.stream):
+            for attr, h in self.inputs.items():
+                self.plan.dm.t[attr].copy_(h, non_blocking=True)
+
+    def download(self):
+        torch = _torch()
+        p = self.plan
+        cap = self.stage.numel()
+        with torch.cuda.stream(p.stream):
+            for t in (p.row_ptr, p.col_idx, p.values, p.rhs):
+                flat = t.reshape(-1).view(torch.uint8)
+                for a in range(0, flat.numel(), cap):
+                    b = min(a + cap, flat.numel())
+                    self.stage[: b - a].copy_(flat[a:b], non_blocking=True)
+
+
 @dataclass
 class DeviceAssembly:
     """Device-resident result of one assembly (CSR in HBM)."""

@@ -580,7 +580,7 @@ cudaError_t launch_assemble(const pdg_mesh& m, const pdg_basis& B, const pdg_coe
   const int64_t grid = std::min<int64_t>(blocks_needed, (int64_t)num_sms() * per_sm * 8);
   if (grid <= 0) return cudaSuccess;
   kern<<<(unsigned)grid, threads, smem, st>>>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs,
-                                               flags, lay, mode);
+                                               flags, lay, mode); note_launch();
   return cudaGetLastError();
 }
 

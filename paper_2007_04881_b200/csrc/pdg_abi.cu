@@ -1,4 +1,5 @@
 // C-ABI entry points, error state and the unit-level debug kernels.
+#include <atomic>
 #include <cstring>
 
 #include "assemble_kernel.cuh"
@@ -6,6 +7,9 @@
 namespace pdg {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
@@ -105,7 +109,7 @@ static cudaError_t launch_tabulate(int P, const pdg_basis& B, int32_t el, const 
                                    double* vals, double* grads, cudaStream_t st) {
   const int grid = grid_for(n, 128);
 #define PDG_TAB(PP) \
-  case PP: tabulate_kernel<DIM, PP><<<grid, 128, 0, st>>>(B, el, pts, n, vals, grads); break;
+  case PP: tabulate_kernel<DIM, PP><<<grid, 128, 0, st>>>(B, el, pts, n, vals, grads); note_launch(); break;
   switch (P) {
     PDG_TAB(0) PDG_TAB(1) PDG_TAB(2) PDG_TAB(3) PDG_TAB(4)
     PDG_TAB(5) PDG_TAB(6)
@@ -120,6 +124,8 @@ static cudaError_t launch_tabulate(int P, const pdg_basis& B, int32_t el, const 
 using namespace pdg;
 
 extern "C" int pdg_abi_version(void) { return PDG_ABI_VERSION; }
+
+extern "C" int64_t pdg_launch_count(void) { return (int64_t)g_launches.load(); }
 
 extern "C" const char* pdg_last_error(void) { return g_last_error.c_str(); }
 
@@ -188,6 +194,7 @@ extern "C" int pdg_map_simplices(const pdg_mesh* mesh, const pdg_rules* rules, i
       map_simplices_kernel<3><<<grid, 128, 0, st>>>(*mesh, *rules, order, simplex_ids, n, points, weights, err_flags);
     else
       return fail(PDG_ERR_UNSUPPORTED, "dim must be 2 or 3");
+    note_launch();
     PDG_CUDA(cudaGetLastError());
     return PDG_OK;
   }

@@ -100,10 +100,10 @@ size_t scan_workspace_bytes(int64_t n) {
 cudaError_t exclusive_scan(const int64_t* in, int64_t n, int64_t* out, int64_t* ws,
                            cudaStream_t st) {
   const int64_t tiles = n > 0 ? (n + SCAN_TILE - 1) / SCAN_TILE : 1;
-  if (n > 0) scan_tile_sums<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, n, ws);
+  if (n > 0) { scan_tile_sums<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, n, ws); note_launch(); }
   else cudaMemsetAsync(ws, 0, sizeof(int64_t), st);
-  scan_tile_offsets<<<1, SCAN_THREADS, 0, st>>>(ws, tiles);
-  scan_apply<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, n, ws, out);
+  scan_tile_offsets<<<1, SCAN_THREADS, 0, st>>>(ws, tiles); note_launch();
+  scan_apply<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, n, ws, out); note_launch();
   return cudaGetLastError();
 }
 
@@ -227,13 +227,15 @@ extern "C" int pdg_adjacency(const pdg_mesh* mesh, int64_t* nbr_ptr, int32_t* nb
     int64_t* cursor = count + (nel + 1);
     int64_t* scan_ws = cursor + (nel + 1);
     const int grid = grid_for(nel);
-    adj_count<<<grid, 256, 0, st>>>(*mesh, count);
-    if (mesh->n_interfaces > 0) adj_count_ifaces<<<grid_for(mesh->n_interfaces), 256, 0, st>>>(*mesh, count);
+    adj_count<<<grid, 256, 0, st>>>(*mesh, count); note_launch();
+    if (mesh->n_interfaces > 0) { adj_count_ifaces<<<grid_for(mesh->n_interfaces), 256, 0, st>>>(*mesh, count); note_launch(); }
     PDG_CUDA(exclusive_scan(count, nel, nbr_ptr, scan_ws, st));
-    adj_fill_self<<<grid, 256, 0, st>>>(*mesh, nbr_ptr, nbr_elem, nbr_iface, cursor);
-    if (mesh->n_interfaces > 0)
+    adj_fill_self<<<grid, 256, 0, st>>>(*mesh, nbr_ptr, nbr_elem, nbr_iface, cursor); note_launch();
+    if (mesh->n_interfaces > 0) {
       adj_fill_ifaces<<<grid_for(mesh->n_interfaces), 256, 0, st>>>(*mesh, nbr_elem, nbr_iface, cursor);
-    adj_sort<<<grid, 128, 0, st>>>(*mesh, nbr_ptr, nbr_elem, nbr_iface);
+      note_launch();
+    }
+    adj_sort<<<grid, 128, 0, st>>>(*mesh, nbr_ptr, nbr_elem, nbr_iface); note_launch();
     PDG_CUDA(cudaGetLastError());
     return PDG_OK;
   }
@@ -252,10 +254,10 @@ extern "C" int pdg_pattern_offsets(const pdg_mesh* mesh, const pdg_basis* basis,
     int64_t* vals = (int64_t*)workspace;
     int64_t* rows = vals + (mesh->n_elements + 1);
     int64_t* scan_ws = rows + (mesh->n_elements + 1);
-    pattern_counts<<<grid_for(nr), 256, 0, st>>>(*basis, *pattern, vals, rows);
+    pattern_counts<<<grid_for(nr), 256, 0, st>>>(*basis, *pattern, vals, rows); note_launch();
     PDG_CUDA(exclusive_scan(vals, nr, pattern->elem_val_offset, scan_ws, st));
     PDG_CUDA(exclusive_scan(rows, nr, pattern->elem_row_offset, scan_ws, st));
-    if (nr > 0) pattern_row_ptr<<<grid_for(nr), 256, 0, st>>>(*basis, *pattern);
+    if (nr > 0) { pattern_row_ptr<<<grid_for(nr), 256, 0, st>>>(*basis, *pattern); note_launch(); }
     else PDG_CUDA(cudaMemsetAsync(pattern->row_ptr, 0, sizeof(int64_t), st));
     PDG_CUDA(cudaGetLastError());
     if (nnz_host) {  // size query: one synchronisation to size col_idx / values
@@ -279,7 +281,7 @@ extern "C" int pdg_pattern_fill(const pdg_mesh* mesh, const pdg_basis* basis,
     if (!mesh || !basis || !pattern || !pattern->col_idx) return fail(PDG_ERR_INVALID, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t nr = pattern->n_row_elements;
-    if (nr > 0) pattern_fill_cols<<<grid_for_warps(nr, 256), 256, 0, st>>>(*basis, *pattern);
+    if (nr > 0) { pattern_fill_cols<<<grid_for_warps(nr, 256), 256, 0, st>>>(*basis, *pattern); note_launch(); }
     PDG_CUDA(cudaGetLastError());
     return PDG_OK;
   }

@@ -28,6 +28,9 @@ int fail(int code, const std::string& msg);
 
 int num_sms();
 
+// launch accounting (pdg_launch_count): every kernel launch site calls this
+void note_launch();
+
 // grid-stride launches: a multiple of the SM count, capped by the work
 inline int grid_for(int64_t n, int threads = 256) {
   const int64_t need = (n + threads - 1) / threads;

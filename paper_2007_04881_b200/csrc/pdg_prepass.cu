@@ -216,19 +216,27 @@ extern "C" int pdg_face_prepass(const pdg_mesh* mesh, const pdg_basis* basis, co
     const bool iso_var = coeffs->diffusion_kind == PDG_DIFF_ISO && !coeffs->diffusion[0].is_const;
     if (iso_var && !elem_abar) return fail(PDG_ERR_INVALID, "elem_abar scratch required");
     if (mesh->dim == 2) {
-      if (iso_var && mesh->n_elements > 0)
+      if (iso_var && mesh->n_elements > 0) {
         elem_abar_iso<2><<<grid_for_warps(mesh->n_elements, 256), 256, 0, st>>>(
             *mesh, *basis, *coeffs, *rules, *params, elem_abar, err_flags);
-      if (mesh->n_faces > 0)
+        note_launch();
+      }
+      if (mesh->n_faces > 0) {
         face_prepass<2><<<grid_for(mesh->n_faces, 128), 128, 0, st>>>(
             *mesh, *basis, *coeffs, *rules, *params, elem_abar, sigma, face_flow, err_flags);
+        note_launch();
+      }
     } else {
-      if (iso_var && mesh->n_elements > 0)
+      if (iso_var && mesh->n_elements > 0) {
         elem_abar_iso<3><<<grid_for_warps(mesh->n_elements, 256), 256, 0, st>>>(
             *mesh, *basis, *coeffs, *rules, *params, elem_abar, err_flags);
-      if (mesh->n_faces > 0)
+        note_launch();
+      }
+      if (mesh->n_faces > 0) {
         face_prepass<3><<<grid_for(mesh->n_faces, 128), 128, 0, st>>>(
             *mesh, *basis, *coeffs, *rules, *params, elem_abar, sigma, face_flow, err_flags);
+        note_launch();
+      }
     }
     PDG_CUDA(cudaGetLastError());
     return PDG_OK;
