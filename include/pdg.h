@@ -24,8 +24,18 @@
 #ifndef PDG_H_
 #define PDG_H_
 
+#ifdef __CUDACC_RTC__ /* runtime-compiled (NVRTC) specialisations see only this */
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long size_t;
+#else
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -153,6 +163,21 @@ typedef struct pdg_pattern {
   int64_t* col_idx;            /* [nnz] */
 } pdg_pattern;
 
+/* Affine frames, produced once per assembly by pdg_frames_build and read by
+ * the element kernel (one broadcast load per quadrature point):
+ *   simplex [n_simplices][W] in ELEMENT order (row elem_ptr[e]+k is the k-th
+ *           simplex of element e): v0, E rows (v_k - v_0), |det E|
+ *           (quadrature.py:118-136);
+ *   facet   [n_facets][W]: v0, E rows, sqrt(det(E E^T)) (quadrature.py:139-156);
+ *   element [n_elements][W]: box centre, 1/half-width, 1/sqrt(width) per axis
+ *           (basis.py:139-152).
+ * W = 8 doubles in 2D, 16 in 3D. */
+typedef struct pdg_frames {
+  double* simplex;
+  double* facet;
+  double* element;
+} pdg_frames;
+
 int pdg_abi_version(void);
 const char* pdg_last_error(void);
 
@@ -191,6 +216,11 @@ int pdg_face_prepass(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coe
                      int8_t* face_flow, double* elem_abar, uint32_t* err_flags,
                      pdg_stream stream);
 
+/* Geometry pre-pass: fills pdg_frames; degenerate simplices / facets raise
+ * PDG_FLAG_DEGENERATE_* (quadrature.py:133-134,152-153). */
+int pdg_frames_build(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_frames* frames,
+                     uint32_t* err_flags, pdg_stream stream);
+
 /* Main kernel: every owned element computes its volume term, the traces of
  * all its faces (both sides, one-sided emission), its boundary terms and its
  * load, and writes its n_e rows of the CSR values (exclusive writer, no
@@ -199,9 +229,26 @@ int pdg_face_prepass(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coe
  * (assembly.py:912-972,1117-1122). */
 int pdg_assemble(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
                  const pdg_rules* rules, const pdg_params* params,
-                 const pdg_pattern* pattern, const double* sigma, const int8_t* face_flow,
-                 double* values, int32_t write_col_idx, double* rhs, uint32_t* err_flags,
-                 pdg_stream stream);
+                 const pdg_pattern* pattern, const pdg_frames* frames, const double* sigma,
+                 const int8_t* face_flow, double* values, int32_t write_col_idx, double* rhs,
+                 uint32_t* err_flags, pdg_stream stream);
+
+/* Same as pdg_assemble, but with the coefficient fields given as CUDA source
+ * of a policy class (generated by paper_2007_04881_b200/model.py from the
+ * same expressions as pdg_coeffs): the element kernel is specialised at run
+ * time with NVRTC for sm_100a (fields inlined, kind flags compile-time
+ * constants) and cached per (source, dim, degree).  `coeffs` is still
+ * required (kind flags for the launch geometry). */
+int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                     const char* policy_source, const pdg_rules* rules, const pdg_params* params,
+                     const pdg_pattern* pattern, const pdg_frames* frames, const double* sigma,
+                     const int8_t* face_flow, double* values, int32_t write_col_idx, double* rhs,
+                     uint32_t* err_flags, pdg_stream stream);
+
+/* Compile (or fetch from the cache) the specialisation pdg_assemble_jit would
+ * use; lets callers pay the NVRTC cost outside timed regions. */
+int pdg_jit_prepare(const pdg_coeffs* coeffs, const char* policy_source, int32_t dim,
+                    int32_t max_degree);
 
 /* ---- unit-level entry points (tests / debugging) ---- */
 
@@ -220,7 +267,7 @@ int pdg_tabulate(const pdg_mesh* mesh, const pdg_basis* basis, int32_t element,
 /* Dense per-element volume blocks [n][nb][nb] and loads [n][nb]
  * (assembly.py:1139-1152); nb = num_basis(max_degree). */
 int pdg_element_blocks(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
-                       const pdg_rules* rules, const pdg_params* params,
+                       const pdg_rules* rules, const pdg_params* params, const pdg_frames* frames,
                        const int32_t* elements, int64_t n, double* blocks, double* loads,
                        uint32_t* err_flags, pdg_stream stream);
 

@@ -82,9 +82,14 @@ class Pattern(C.Structure):
                 ("row_ptr", _p), ("col_idx", _p)]
 
 
+class Frames(C.Structure):
+    _fields_ = [("simplex", _p), ("facet", _p), ("element", _p)]
+
+
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
 EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes", "pdg_adjacency",
-           "pdg_pattern_offsets", "pdg_pattern_fill", "pdg_face_prepass", "pdg_assemble",
+           "pdg_pattern_offsets", "pdg_pattern_fill", "pdg_face_prepass", "pdg_frames_build",
+           "pdg_assemble", "pdg_assemble_jit", "pdg_jit_prepare",
            "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks")
 
 
@@ -111,12 +116,16 @@ def load():
     lib.pdg_pattern_fill.argtypes = [P(Mesh), P(Basis), P(Pattern), _p]
     lib.pdg_face_prepass.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params),
                                      _p, _p, _p, _p, _p]
+    lib.pdg_frames_build.argtypes = [P(Mesh), P(Basis), P(Frames), _p, _p]
     lib.pdg_assemble.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params), P(Pattern),
-                                 _p, _p, _p, _i32, _p, _p, _p]
+                                 P(Frames), _p, _p, _p, _i32, _p, _p, _p]
+    lib.pdg_assemble_jit.argtypes = [P(Mesh), P(Basis), P(Coeffs), C.c_char_p, P(Rules), P(Params),
+                                     P(Pattern), P(Frames), _p, _p, _p, _i32, _p, _p, _p]
+    lib.pdg_jit_prepare.argtypes = [P(Coeffs), C.c_char_p, _i32, _i32]
     lib.pdg_map_simplices.argtypes = [P(Mesh), P(Rules), _i32, _p, _i64, _p, _p, _p, _p]
     lib.pdg_tabulate.argtypes = [P(Mesh), P(Basis), _i32, _p, _i64, _p, _p, _p]
-    lib.pdg_element_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params), _p,
-                                       _i64, _p, _p, _p, _p]
+    lib.pdg_element_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params),
+                                       P(Frames), _p, _i64, _p, _p, _p, _p]
     for name in EXPORTS:
         if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes"):
             getattr(lib, name).restype = C.c_int

@@ -18,7 +18,9 @@ maps device error flags to polydg's exception classes.  No CPU fallback.
 
 from __future__ import annotations
 
+import os
 import time
+import warnings
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -27,7 +29,7 @@ import numpy as np
 from . import _lib
 from .basis import family_name, num_basis, spec_arrays
 from .mesh import BOUNDARY, TAG_CODE, FlatMesh, MeshError, flat_of
-from .model import ClassificationError, PenaltyConfig, compile_coeffs
+from .model import ClassificationError, PenaltyConfig, compile_coeffs, policy_source
 from .quadrature import QuadratureError, RuleTable
 
 KERNEL_NAMES = ("element", "interior", "dirichlet", "inflow", "neumann_outflow")
@@ -361,7 +363,9 @@ class SipgPlan:
     """
 
     def __init__(self, mesh, coeffs, specs, config: Optional[AssemblyConfig] = None,
-                 row_elements=None, device=None, stream=None):
+                 row_elements=None, device=None, stream=None, jit: bool = True):
+        import ctypes as C
+
         torch = _torch()
         self.lib = _lib.load()
         config = config or AssemblyConfig()
@@ -406,6 +410,17 @@ class SipgPlan:
 
         self.cdesc = compile_coeffs(coeffs, d)
         self.coeffs = _lib.coeffs_struct(self.cdesc)
+        self.jit_source = None
+        self.kernel_variant = "aot-interpreted"
+        if jit and os.environ.get("PDG_JIT", "1") != "0":
+            src = policy_source(coeffs, d).encode()
+            rc = self.lib.pdg_jit_prepare(C.byref(self.coeffs), src, d, pmax)
+            if rc == _lib.PDG_OK:
+                self.jit_source = src
+                self.kernel_variant = "nvrtc-specialised"
+            else:
+                warnings.warn("runtime specialisation unavailable, using the ahead-of-time kernel: "
+                              + self.lib.pdg_last_error().decode(errors="replace"))
         prm = _lib.Params()
         prm.quad_increment = inc
         prm.include_gradient_terms = 1
@@ -434,6 +449,14 @@ class SipgPlan:
                       row_ptr=z(self.n_local_rows + 1, i64),
                       sigma=z(flat.n_faces, torch.float64), flow=z(flat.n_faces, torch.int8),
                       abar=z(nel, torch.float64), flags=torch.zeros(1, dtype=torch.int32, device=dev))
+        W = 8 if d == 2 else 16
+        self.t.update(sframe=z(flat.n_simplices * W, torch.float64),
+                      fframe=z(flat.n_facets * W, torch.float64),
+                      erec=z(nel * W, torch.float64))
+        fr = _lib.Frames()
+        fr.simplex, fr.facet, fr.element = (_lib.ptr(self.t["sframe"]), _lib.ptr(self.t["fframe"]),
+                                            _lib.ptr(self.t["erec"]))
+        self.frames = fr
         self.ws_bytes = int(self.lib.pdg_workspace_bytes(nel, flat.n_interfaces))
         self.t["ws"] = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
         pat = _lib.Pattern()
@@ -475,6 +498,9 @@ class SipgPlan:
     def _prepass(self):
         import ctypes as C
 
+        _lib.check(self.lib.pdg_frames_build(C.byref(self.dm.struct), C.byref(self.basis),
+                                             C.byref(self.frames), _lib.ptr(self.t["flags"]),
+                                             _lib.stream_ptr(self.stream)))
         _lib.check(self.lib.pdg_face_prepass(
             C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs),
             C.byref(self.rules.struct), C.byref(self.params), _lib.ptr(self.t["sigma"]),
@@ -484,12 +510,15 @@ class SipgPlan:
     def _elements(self, write_col_idx=True):
         import ctypes as C
 
-        _lib.check(self.lib.pdg_assemble(
-            C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs),
-            C.byref(self.rules.struct), C.byref(self.params), C.byref(self.pattern),
-            _lib.ptr(self.t["sigma"]), _lib.ptr(self.t["flow"]), _lib.ptr(self.t["values"]),
-            1 if write_col_idx else 0, _lib.ptr(self.t["rhs"]), _lib.ptr(self.t["flags"]),
-            _lib.stream_ptr(self.stream)))
+        tail = (C.byref(self.rules.struct), C.byref(self.params), C.byref(self.pattern),
+                C.byref(self.frames), _lib.ptr(self.t["sigma"]), _lib.ptr(self.t["flow"]),
+                _lib.ptr(self.t["values"]), 1 if write_col_idx else 0, _lib.ptr(self.t["rhs"]),
+                _lib.ptr(self.t["flags"]), _lib.stream_ptr(self.stream))
+        head = (C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs))
+        if self.jit_source is not None:
+            _lib.check(self.lib.pdg_assemble_jit(*head, self.jit_source, *tail))
+        else:
+            _lib.check(self.lib.pdg_assemble(*head, *tail))
 
     def run(self, events=None):
         """Enqueue index phase + pre-pass + element kernel; no host sync.
@@ -744,9 +773,12 @@ def element_kernel(mesh, element, coeffs, spec, quad_increment=2):
     ids = torch.tensor([int(element)], dtype=torch.int32, device=plan.device)
     blocks = torch.zeros(nb * nb, dtype=torch.float64, device=plan.device)
     loads = torch.zeros(nb, dtype=torch.float64, device=plan.device)
+    _lib.check(plan.lib.pdg_frames_build(C.byref(plan.dm.struct), C.byref(plan.basis),
+                                         C.byref(plan.frames), _lib.ptr(plan.flags),
+                                         _lib.stream_ptr(plan.stream)))
     _lib.check(plan.lib.pdg_element_blocks(
         C.byref(plan.dm.struct), C.byref(plan.basis), C.byref(plan.coeffs),
-        C.byref(plan.rules.struct), C.byref(plan.params), _lib.ptr(ids), 1,
+        C.byref(plan.rules.struct), C.byref(plan.params), C.byref(plan.frames), _lib.ptr(ids), 1,
         _lib.ptr(blocks), _lib.ptr(loads), _lib.ptr(plan.flags), _lib.stream_ptr(plan.stream)))
     plan.stream.synchronize()
     _raise_flags(int(plan.flags.item()))
@@ -781,3 +813,11 @@ class _UnitPlan:
         self.params.penalty_constant = 10.0
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.stream = torch.cuda.current_stream(self.device)
+        f = self.dm.flat
+        W = 8 if d == 2 else 16
+        mk = lambda n: torch.empty(max(int(n) * W, 1), dtype=torch.float64, device=self.device)
+        self.t.update(sframe=mk(f.n_simplices), fframe=mk(f.n_facets), erec=mk(f.n_elements))
+        fr = _lib.Frames()
+        fr.simplex, fr.facet, fr.element = (_lib.ptr(self.t["sframe"]), _lib.ptr(self.t["fframe"]),
+                                            _lib.ptr(self.t["erec"]))
+        self.frames = fr

@@ -1,0 +1,648 @@
+// The element kernel body: one warp owns one row element and produces all of
+// its CSR rows and its RHS segment in a single pass.
+//
+//   volume    K_e  += sum_q w [ (A grad phi_j).grad phi_i + (b.grad phi_j) phi_i + c phi_j phi_i ]
+//                                                        (polydg assembly.py:396-415)
+//   faces     rows of e of the SIPG interior blocks     (assembly.py:418-463)
+//             with both traces evaluated here, so every value slot has exactly
+//             one writer (no atomics, no zero-fill pass, bitwise deterministic,
+//             and a row-partitioned run reproduces the one-sided cut-face
+//             semantics of assembly.py:685-696,778-788 for free)
+//   boundary  Dirichlet / inflow / Neumann terms         (assembly.py:466-512)
+//
+// Every term is a sum of rank-1 updates C += L R^T over "items" (one per
+// quadrature point and term), contracted with DMMA m8n8k4 (SASS DMMA.8x8x4):
+//   volume   ISO   L = w a dphi/dx_c,   R = dphi/dx_c              (c < d)
+//            FULL  L = w dphi/dx_c,     R = (A grad phi)_c
+//            b/c   L = w phi,           R = b.grad phi + c phi
+//   face     L1 = alpha V_a + beta F_a, L2 = beta V_a, with
+//            alpha = w sigma - s_a [e downwind] w b.n,  beta = -1/2 s_a w,
+//            diag  C_aa += L1 V_a^T + L2 F_a^T,  off  C_ab += L1 (-V_b)^T + L2 F_b^T
+//   (F = n_owner . A grad phi; derivation in DESIGN.md §3).
+//
+// Quadrature points are tabulated lane-parallel (one lane = one point) into a
+// per-warp shared-memory table laid out [row][function][slot] with a slot
+// stride = 4 (mod 16) doubles, so both the tabulation stores (consecutive
+// slots) and the DMMA fragment loads (8 functions x 4 slots) are bank-conflict
+// free.  Geometry arrives pre-mapped: per-simplex / per-facet affine frames
+// and per-element basis constants are produced once per assembly by
+// geometry_frames (pdg_prepass.cu), so a quadrature point costs one broadcast
+// load of its frame instead of three dependent gathers.
+//
+// The coefficient fields enter through a policy class CF: the ahead-of-time
+// library uses InterpCoef (bytecode interpreter over pdg_coeffs); the runtime
+// specialisation (pdg_jit.cu, NVRTC) passes a generated class whose fields are
+// inlined expressions and whose kind flags are compile-time constants.
+#pragma once
+
+#include "sipg_device.cuh"
+
+namespace pdg {
+
+constexpr int KF = 16;   // face slots per round
+constexpr int KFP = 20;  // face slot stride
+constexpr int NBR_WIN = 32;  // neighbour entries staged per window
+
+template <int DIM>
+struct Widths {
+  static constexpr int SF = DIM == 2 ? 8 : 16;  // simplex frame: v0, E (row-major), |det|
+  static constexpr int FF = DIM == 2 ? 8 : 16;  // facet frame: v0, E rows, sqrt(det(EE^T))
+  static constexpr int ER = DIM == 2 ? 8 : 16;  // element record: centre, 1/half, 1/sqrt(width)
+};
+
+struct AsmLayout {
+  int kv;            // volume slots per round (16 or 32)
+  int vrows;         // volume table rows
+  int warp_doubles;  // per-warp shared memory (doubles)
+  int buf_doubles;   // table part of it (scalars + staging follow)
+};
+
+struct KArgs {
+  pdg_mesh m;
+  pdg_basis B;
+  pdg_rules R;
+  pdg_params prm;
+  pdg_pattern pat;
+  const double* sigma;
+  const int8_t* flow;
+  const double* sframe;  // [n_simplices][SF], element order (elem_ptr indexing)
+  const double* fframe;  // [n_facets][FF]
+  const double* erec;    // [n_elements][ER]
+  double* values;
+  double* rhs;
+  uint32_t* flags;
+  int write_cols;
+  int mode;  // 0: CSR rows; 1: dense volume-only blocks (unit entry point)
+  AsmLayout lay;
+};
+
+template <int DIM, int P>
+struct Shape {
+  static constexpr int NB = binom(P + DIM, DIM);
+  static constexpr int NT = (NB + 7) / 8;
+  static constexpr int NBP = NT * 8;
+  static constexpr bool RHS_REGS = NB <= 20;
+};
+
+// per-warp staging of the neighbour window (ints) -- after the scalars
+struct NbrStage {
+  int j[NBR_WIN], nj[NBR_WIN], col[NBR_WIN], fa[NBR_WIN], fb[NBR_WIN], pj[NBR_WIN];
+};
+
+// Ahead-of-time coefficient policy: interprets the bytecode in pdg_coeffs.
+template <int DIM>
+struct InterpCoef {
+  const pdg_coeffs& C;
+  __device__ InterpCoef(const pdg_coeffs& c) : C(c) {}
+  __device__ int diff_kind() const { return C.diffusion_kind; }
+  __device__ bool has_adv() const { return C.has_advection; }
+  __device__ bool has_reac() const { return C.has_reaction; }
+  __device__ bool has_src() const { return C.has_source; }
+  __device__ bool has_dir() const { return C.has_dirichlet; }
+  __device__ bool has_neu() const { return C.has_neumann; }
+  __device__ double a_iso(const double* x) const { return eval_prog(C, C.diffusion[0], x); }
+  __device__ double a_ij(int i, int j, const double* x) const { return eval_prog(C, C.diffusion[i * DIM + j], x); }
+  __device__ double b_i(int i, const double* x) const { return eval_prog(C, C.advection[i], x); }
+  __device__ double c(const double* x) const { return eval_prog(C, C.reaction, x); }
+  __device__ double f(const double* x) const { return eval_prog(C, C.source, x); }
+  __device__ double gD(const double* x) const { return eval_prog(C, C.dirichlet, x); }
+  __device__ double gN(const double* x) const { return eval_prog(C, C.neumann, x); }
+};
+
+template <int DIM>
+__device__ __forceinline__ BoxConst<DIM> load_box(const double* erec, int64_t e) {
+  const double* r = erec + e * Widths<DIM>::ER;
+  BoxConst<DIM> b;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    b.c[i] = r[i];
+    b.ih[i] = r[DIM + i];
+    b.rs[i] = r[2 * DIM + i];
+  }
+  return b;
+}
+
+// x = v0 + xi E from a frame record (v0 then E rows), returns the stored measure
+template <int DIM, int K>
+__device__ __forceinline__ double frame_point(const double* fr, const double* xi, double* x) {
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    double acc = fr[i];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc += xi[j] * fr[DIM + j * DIM + i];
+    x[i] = acc;
+  }
+  return fr[DIM + K * DIM];
+}
+
+// Store one C tile set into rows of the element's row block (optionally
+// with its mirror image for symmetric accumulation).
+template <int NT, bool SYM>
+__device__ __forceinline__ void store_block(double* values, int64_t voff, int64_t L, int64_t col0, int ne,
+                                            int nj, const double (&c)[NT][NT][2], int g, int t) {
+#pragma unroll
+  for (int r = 0; r < NT; ++r) {
+#pragma unroll
+    for (int cc = 0; cc < NT; ++cc) {
+      if (SYM && cc < r) continue;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = r * 8 + g, j = cc * 8 + 2 * t + u;
+        if (i < ne && j < nj) values[voff + (int64_t)i * L + col0 + j] = c[r][cc][u];
+        if (SYM && cc > r && j < ne && i < nj) values[voff + (int64_t)j * L + col0 + i] = c[r][cc][u];
+      }
+    }
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void zero_tiles(double (&c)[NT][NT][2]) {
+#pragma unroll
+  for (int r = 0; r < NT; ++r)
+#pragma unroll
+    for (int cc = 0; cc < NT; ++cc) c[r][cc][0] = c[r][cc][1] = 0.0;
+}
+
+// Face trace values at one point: V_f and the flux F_f = n.(A grad phi_f)
+template <int DIM, int P, class CF>
+__device__ __forceinline__ double face_flux(const CF& cf, const Tab<DIM, P>& tb, int f, const double* nrm,
+                                            double a, const double (&A)[DIM][DIM]) {
+  double fl = 0.0;
+  if (cf.diff_kind() == PDG_DIFF_FULL) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      double ag = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < DIM; ++jj) ag += A[i][jj] * tb.grad(f, jj);
+      fl += nrm[i] * ag;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) fl += nrm[i] * tb.grad(f, i);
+    fl *= a;
+  }
+  return fl;
+}
+
+template <int DIM, int P, bool SYM, class CF>
+__device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
+  using S = Shape<DIM, P>;
+  using W = Widths<DIM>;
+  constexpr int NB = S::NB, NT = S::NT, NBP = S::NBP;
+  extern __shared__ double smem[];
+  const pdg_mesh& m = a.m;
+  const pdg_basis& B = a.B;
+  const pdg_rules& R = a.R;
+  const pdg_pattern& pat = a.pat;
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double* buf = smem + (threadIdx.x >> 5) * a.lay.warp_doubles;
+  double* sc1 = buf + a.lay.buf_doubles;
+  double* sc2 = sc1 + 32;
+  NbrStage* ns = reinterpret_cast<NbrStage*>(sc2 + 32);
+  double* rhs_s = reinterpret_cast<double*>(ns + 1);  // [NB][32] when !RHS_REGS
+
+  const int kv = a.lay.kv, kvp = a.lay.kv + 4;
+  const int dk = cf.diff_kind();
+  const int nG = dk != PDG_DIFF_NONE ? DIM : 0;
+  const bool full = dk == PDG_DIFF_FULL;
+  const bool has_vr = cf.has_adv() || cf.has_reac();
+  const int rAG = nG, rV = nG + (full ? DIM : 0), rR = rV + 1;
+  const bool grad_terms = dk != PDG_DIFF_NONE && a.prm.include_gradient_terms;
+  const int mode = a.mode;
+
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < pat.n_row_elements;
+       k += nwarps) {
+    const int32_t e = pat.row_elements ? pat.row_elements[k] : (int32_t)k;
+    const int pe = B.degree[e];
+    const int64_t dof_e = B.dof_offset[e];
+    const int ne = (int)(B.dof_offset[e + 1] - dof_e);
+    const BoxConst<DIM> bx = load_box<DIM>(a.erec, e);
+    const int64_t voff = mode ? k * NB * NB : pat.elem_val_offset[k];
+    const int64_t Lrow = mode ? NB : pat.row_len[k];
+
+    double cd[NT][NT][2];
+    zero_tiles<NT>(cd);
+    double racc[S::RHS_REGS ? NB : 1];
+#pragma unroll
+    for (int f = 0; f < (S::RHS_REGS ? NB : 1); ++f) racc[f] = 0.0;
+    if (!S::RHS_REGS)
+      for (int f = 0; f < NB; ++f) rhs_s[f * 32 + lane] = 0.0;
+    auto rhs_add = [&](int f, double v) {
+      if constexpr (S::RHS_REGS) racc[f] += v;
+      else rhs_s[f * 32 + lane] += v;
+    };
+
+    // ------------------------------------------------------------ volume
+    {
+      const int order = 2 * pe + a.prm.quad_increment;
+      const int r0 = R.vol_offset[order], nq = R.vol_count[order];
+      const int64_t s0 = m.elem_ptr[e];
+      const int Q = (int)(m.elem_ptr[e + 1] - s0) * nq;
+      for (int base = 0; base < Q; base += kv) {
+        const int nvalid = min(kv, Q - base);
+        if (lane < kv) {
+          const int gq = base + min(lane, nvalid - 1);
+          const double valid = lane < nvalid ? 1.0 : 0.0;
+          const int ls = gq / nq;
+          const int kq = gq - ls * nq;
+          const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+          double x[3] = {0.0, 0.0, 0.0};
+          const double det = frame_point<DIM, DIM>(a.sframe + (s0 + ls) * W::SF, xi, x);
+          const double w = R.weights[r0 + kq] * det * valid;
+          Tab<DIM, P> tb;
+          tb.load(bx, x);
+          double* col = buf + lane;
+          if (nG) {
+            const double av = dk == PDG_DIFF_ISO ? cf.a_iso(x) : 1.0;
+            sc1[lane] = w * av;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c)
+#pragma unroll
+              for (int f = 0; f < NBP; ++f) col[(c * NBP + f) * kvp] = f < NB ? tb.grad(f, c) : 0.0;
+            if (full) {
+              double A[DIM][DIM];
+#pragma unroll
+              for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                for (int j = 0; j < DIM; ++j) A[i][j] = cf.a_ij(i, j, x);
+#pragma unroll
+              for (int c = 0; c < DIM; ++c)
+#pragma unroll
+                for (int f = 0; f < NBP; ++f) {
+                  double v = 0.0;
+                  if (f < NB) {
+#pragma unroll
+                    for (int j = 0; j < DIM; ++j) v += A[c][j] * tb.grad(f, j);
+                  }
+                  col[((rAG + c) * NBP + f) * kvp] = v;
+                }
+            }
+          }
+          if (has_vr) {
+            sc2[lane] = w;
+            double bvec[DIM];
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) bvec[i] = cf.has_adv() ? cf.b_i(i, x) : 0.0;
+            const double cr = cf.has_reac() ? cf.c(x) : 0.0;
+#pragma unroll
+            for (int f = 0; f < NBP; ++f) {
+              double vv = 0.0, rr = 0.0;
+              if (f < NB) {
+                vv = tb.val(f);
+                if (cf.has_adv()) {
+#pragma unroll
+                  for (int i = 0; i < DIM; ++i) rr += bvec[i] * tb.grad(f, i);
+                }
+                if (cf.has_reac()) rr += cr * vv;
+              }
+              col[(rV * NBP + f) * kvp] = vv;
+              col[(rR * NBP + f) * kvp] = rr;
+            }
+          }
+          if (cf.has_src()) {
+            const double wf = w * cf.f(x);
+#pragma unroll
+            for (int f = 0; f < NB; ++f) rhs_add(f, wf * tb.val(f));
+          }
+        }
+        __syncwarp();
+        const int nk = (nvalid + 3) >> 2;
+        for (int kk = 0; kk < nk; ++kk) {
+          const int q = kk * 4 + t;
+          if (nG) {
+            const double s1 = sc1[q];
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+              double lf[NT], rf[NT];
+#pragma unroll
+              for (int i = 0; i < NT; ++i) {
+                const double gv = buf[(c * NBP + i * 8 + g) * kvp + q];
+                lf[i] = s1 * gv;
+                rf[i] = full ? buf[((rAG + c) * NBP + i * 8 + g) * kvp + q] : gv;
+              }
+#pragma unroll
+              for (int r = 0; r < NT; ++r)
+#pragma unroll
+                for (int cc = 0; cc < NT; ++cc)
+                  if (!SYM || cc >= r) dmma(cd[r][cc], lf[r], rf[cc]);
+            }
+          }
+          if (has_vr) {
+            const double s2 = sc2[q];
+            double lf[NT], rf[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+              lf[i] = s2 * buf[(rV * NBP + i * 8 + g) * kvp + q];
+              rf[i] = buf[(rR * NBP + i * 8 + g) * kvp + q];
+            }
+#pragma unroll
+            for (int r = 0; r < NT; ++r)
+#pragma unroll
+              for (int cc = 0; cc < NT; ++cc)
+                if (!SYM || cc >= r) dmma(cd[r][cc], lf[r], rf[cc]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+
+    // ------------------------------------------------------------ interfaces
+    int64_t colself = 0;
+    const int64_t q0 = mode ? 0 : pat.nbr_ptr[e];
+    const int nnb = mode ? 0 : (int)(pat.nbr_ptr[e + 1] - q0);
+    int colcarry = 0;
+    for (int w0 = 0; w0 < nnb; w0 += NBR_WIN) {
+      const int nw = min(NBR_WIN, nnb - w0);
+      // stage the window: neighbour, its DoF count, column start, face range
+      {
+        int nj = 0;
+        if (lane < nw) {
+          const int32_t j = pat.nbr_elem[q0 + w0 + lane];
+          const int32_t ifc = pat.nbr_iface[q0 + w0 + lane];
+          nj = (int)(B.dof_offset[j + 1] - B.dof_offset[j]);
+          ns->j[lane] = j;
+          ns->nj[lane] = nj;
+          ns->pj[lane] = B.degree[j];
+          ns->fa[lane] = ifc >= 0 ? (int)m.iface_ptr[ifc] : 0;
+          ns->fb[lane] = ifc >= 0 ? (int)m.iface_ptr[ifc + 1] : 0;
+        }
+        int incl = nj;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (lane < nw) ns->col[lane] = colcarry + incl - nj;
+        colcarry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      __syncwarp();
+      // col_idx of this window's column span, all rows (division-free)
+      if (a.write_cols) {
+        const int c0 = ns->col[0];
+        const int c1 = ns->col[nw - 1] + ns->nj[nw - 1];
+        for (int p = c0 + lane; p < c1; p += 32) {
+          int q = 0;
+          while (q + 1 < nw && ns->col[q + 1] <= p) ++q;
+          const int64_t cv = B.dof_offset[ns->j[q]] + (p - ns->col[q]);
+          int64_t* dst = pat.col_idx + voff + p;
+          for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
+        }
+      }
+      for (int qi = 0; qi < nw; ++qi) {
+        const int32_t j = ns->j[qi];
+        const int nj = ns->nj[qi];
+        const int colstart = ns->col[qi];
+        if (j == e) {
+          colself = colstart;
+          continue;
+        }
+        const BoxConst<DIM> bo = load_box<DIM>(a.erec, j);
+        const int pj = ns->pj[qi];
+        double co[NT][NT][2];
+        zero_tiles<NT>(co);
+        const int fend = ns->fb[qi];
+        for (int f = ns->fa[qi]; f < fend; ++f) {
+          const int side = m.face_owner[f] == e ? 0 : 1;
+          const double sgn = side == 0 ? 1.0 : -1.0;
+          const double sig = a.sigma[f];
+          const bool down = cf.has_adv() && a.flow[f] == side;
+          const int order = 2 * max(pe, pj) + a.prm.quad_increment;
+          const int r0 = R.face_offset[order], nq = R.face_count[order];
+          double nrm[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)f * DIM + i];
+          const int64_t row0 = m.face_ptr[f];
+          const int Pf = (int)(m.face_ptr[f + 1] - row0) * nq;
+          const bool mine = lane < KF;
+          const int slot = lane & (KF - 1);
+          for (int base = 0; base < Pf; base += KF) {
+            const int nvalid = min(KF, Pf - base);
+            {
+              const int gq = base + min(slot, nvalid - 1);
+              const double valid = slot < nvalid ? 1.0 : 0.0;
+              const int lr = gq / nq;
+              const int kq = gq - lr * nq;
+              const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+              double x[3] = {0.0, 0.0, 0.0};
+              const double jac = frame_point<DIM, DIM - 1>(a.fframe + (row0 + lr) * W::FF, xi, x);
+              const double w = R.weights[r0 + kq] * jac * valid;
+              Tab<DIM, P> tb;
+              tb.load(mine ? bx : bo, x);
+              double av = 1.0;
+              double A[DIM][DIM];
+              if (grad_terms) {
+                if (full) {
+#pragma unroll
+                  for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < DIM; ++jj) A[i][jj] = cf.a_ij(i, jj, x);
+                } else {
+                  av = cf.a_iso(x);
+                }
+              }
+              double* col = buf + slot;
+              const int rv = mine ? 0 : 2;
+              const double vs = mine ? 1.0 : -1.0;
+#pragma unroll
+              for (int ff = 0; ff < NBP; ++ff) {
+                double vv = 0.0, fl = 0.0;
+                if (ff < NB) {
+                  vv = tb.val(ff);
+                  if (grad_terms) fl = face_flux<DIM, P>(cf, tb, ff, nrm, av, A);
+                }
+                col[(rv * NBP + ff) * KFP] = vs * vv;
+                col[((rv + 1) * NBP + ff) * KFP] = fl;
+              }
+              if (mine) {
+                double wbn = 0.0;
+                if (down) {
+                  double bn = 0.0;
+#pragma unroll
+                  for (int i = 0; i < DIM; ++i) bn += cf.b_i(i, x) * nrm[i];
+                  wbn = w * bn;
+                }
+                sc1[slot] = w * sig - sgn * wbn;
+                sc2[slot] = grad_terms ? -0.5 * sgn * w : 0.0;
+              }
+            }
+            __syncwarp();
+            const int nk = (nvalid + 3) >> 2;
+            for (int kk = 0; kk < nk; ++kk) {
+              const int qq = kk * 4 + t;
+              const double al = sc1[qq], be = sc2[qq];
+              double va[NT], fa[NT], nvb[NT], fb[NT], l1[NT], l2[NT];
+#pragma unroll
+              for (int i = 0; i < NT; ++i) {
+                va[i] = buf[(0 * NBP + i * 8 + g) * KFP + qq];
+                nvb[i] = buf[(2 * NBP + i * 8 + g) * KFP + qq];
+                if (grad_terms) {
+                  fa[i] = buf[(1 * NBP + i * 8 + g) * KFP + qq];
+                  fb[i] = buf[(3 * NBP + i * 8 + g) * KFP + qq];
+                  l1[i] = al * va[i] + be * fa[i];
+                  l2[i] = be * va[i];
+                } else {
+                  fa[i] = fb[i] = l2[i] = 0.0;
+                  l1[i] = al * va[i];
+                }
+              }
+#pragma unroll
+              for (int r = 0; r < NT; ++r)
+#pragma unroll
+                for (int cc = 0; cc < NT; ++cc) {
+                  if (!SYM || cc >= r) {
+                    dmma(cd[r][cc], l1[r], va[cc]);
+                    if (grad_terms) dmma(cd[r][cc], l2[r], fa[cc]);
+                  }
+                  dmma(co[r][cc], l1[r], nvb[cc]);
+                  if (grad_terms) dmma(co[r][cc], l2[r], fb[cc]);
+                }
+            }
+            __syncwarp();
+          }
+        }
+        store_block<NT, false>(a.values, voff, Lrow, colstart, ne, nj, co, g, t);
+      }
+      __syncwarp();
+    }
+
+    // ------------------------------------------------------------ boundary faces
+    const int64_t bend = mode ? 0 : m.elem_bface_ptr[e + 1];
+    for (int64_t bi = mode ? 0 : m.elem_bface_ptr[e]; bi < bend; ++bi) {
+      const int32_t f = m.elem_bfaces[bi];
+      const int tag = m.face_tag[f];
+      if (tag == PDG_TAG_OUTFLOW || tag == PDG_TAG_INTERIOR) continue;
+      if (tag == PDG_TAG_NEUMANN && !cf.has_neu()) continue;
+      const bool matrix = tag != PDG_TAG_NEUMANN;
+      const double sig = a.sigma[f];
+      const bool wi = tag == PDG_TAG_DIRICHLET && cf.has_adv() && a.flow[f] == 1;
+      const int order = 2 * pe + a.prm.quad_increment;
+      const int r0 = R.face_offset[order], nq = R.face_count[order];
+      double nrm[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)f * DIM + i];
+      const int64_t row0 = m.face_ptr[f];
+      const int Pf = (int)(m.face_ptr[f + 1] - row0) * nq;
+      const int slot = lane & (KF - 1);
+      const bool mine = lane < KF;
+      const bool use_f = tag == PDG_TAG_DIRICHLET && grad_terms;
+      for (int base = 0; base < Pf; base += KF) {
+        const int nvalid = min(KF, Pf - base);
+        {
+          const int gq = base + min(slot, nvalid - 1);
+          const double valid = (slot < nvalid && mine) ? 1.0 : 0.0;
+          const int lr = gq / nq;
+          const int kq = gq - lr * nq;
+          const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+          double x[3] = {0.0, 0.0, 0.0};
+          const double jac = frame_point<DIM, DIM - 1>(a.fframe + (row0 + lr) * W::FF, xi, x);
+          const double w = R.weights[r0 + kq] * jac * valid;
+          Tab<DIM, P> tb;
+          tb.load(bx, x);
+          double av = 1.0;
+          double A[DIM][DIM];
+          if (use_f) {
+            if (full) {
+#pragma unroll
+              for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                for (int jj = 0; jj < DIM; ++jj) A[i][jj] = cf.a_ij(i, jj, x);
+            } else {
+              av = cf.a_iso(x);
+            }
+          }
+          double wbn = 0.0;
+          if ((wi || tag == PDG_TAG_INFLOW) && cf.has_adv()) {
+            double bn = 0.0;
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) bn += cf.b_i(i, x) * nrm[i];
+            wbn = w * bn;
+          }
+          double al = 0.0, be = 0.0, gval = 0.0;
+          if (tag == PDG_TAG_DIRICHLET) {
+            al = w * sig - (wi ? wbn : 0.0);
+            be = use_f ? -w : 0.0;
+            gval = cf.has_dir() ? cf.gD(x) : 0.0;
+          } else if (tag == PDG_TAG_INFLOW) {
+            al = -wbn;
+            gval = cf.has_dir() ? cf.gD(x) : 0.0;
+          } else {  // Neumann: load only
+            gval = w * cf.gN(x);
+          }
+          double* col = buf + slot;
+#pragma unroll
+          for (int ff = 0; ff < NBP; ++ff) {
+            double vv = 0.0, fl = 0.0;
+            if (ff < NB) {
+              vv = tb.val(ff);
+              if (use_f) fl = face_flux<DIM, P>(cf, tb, ff, nrm, av, A);
+              if (mine) {
+                if (tag == PDG_TAG_NEUMANN) rhs_add(ff, gval * vv);
+                else if (cf.has_dir()) rhs_add(ff, gval * (al * vv + be * fl));
+              }
+            }
+            if (mine && matrix) {
+              col[(0 * NBP + ff) * KFP] = vv;
+              col[(1 * NBP + ff) * KFP] = fl;
+            }
+          }
+          if (mine && matrix) {
+            sc1[slot] = al;
+            sc2[slot] = be;
+          }
+        }
+        __syncwarp();
+        if (matrix) {
+          const int nk = (nvalid + 3) >> 2;
+          for (int kk = 0; kk < nk; ++kk) {
+            const int qq = kk * 4 + t;
+            const double al = sc1[qq], be = sc2[qq];
+            double va[NT], fa[NT], l1[NT], l2[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+              va[i] = buf[(0 * NBP + i * 8 + g) * KFP + qq];
+              fa[i] = buf[(1 * NBP + i * 8 + g) * KFP + qq];
+              l1[i] = al * va[i] + be * fa[i];
+              l2[i] = be * va[i];
+            }
+#pragma unroll
+            for (int r = 0; r < NT; ++r)
+#pragma unroll
+              for (int cc = 0; cc < NT; ++cc)
+                if (!SYM || cc >= r) {
+                  dmma(cd[r][cc], l1[r], va[cc]);
+                  if (use_f) dmma(cd[r][cc], l2[r], fa[cc]);
+                }
+          }
+        }
+        __syncwarp();
+      }
+    }
+
+    // ------------------------------------------------------------ write-out
+    store_block<NT, SYM>(a.values, voff, Lrow, colself, ne, ne, cd, g, t);
+    double* rhs_out = mode ? a.rhs + k * NB : a.rhs + dof_e;
+    __syncwarp();
+    if constexpr (S::RHS_REGS) {
+#pragma unroll
+      for (int f = 0; f < NB; ++f) buf[lane * NB + f] = racc[f];
+      __syncwarp();
+      for (int f = lane; f < ne; f += 32) {
+        double s = 0.0;
+        for (int l = 0; l < 32; ++l) s += buf[l * NB + f];
+        rhs_out[f] = s;
+      }
+    } else {
+      __syncwarp();
+      for (int f = lane; f < ne; f += 32) {
+        double s = 0.0;
+        for (int l = 0; l < 32; ++l) s += rhs_s[f * 32 + l];
+        rhs_out[f] = s;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace pdg

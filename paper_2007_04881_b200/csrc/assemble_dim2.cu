@@ -1,28 +1,25 @@
-// Instantiations of the element kernel for dim 2 (split per dimension so
-// the two translation units compile in parallel).
+// Ahead-of-time instantiations of the element kernel for dim 2 (one
+// translation unit per dimension so they compile in parallel).
 #include "assemble_kernel.cuh"
 
 namespace pdg {
 
-cudaError_t launch_assemble_dim2(int P, bool sym, const pdg_mesh& m, const pdg_basis& B, const pdg_coeffs& C,
-                                 const pdg_rules& R, const pdg_params& prm, const pdg_pattern& pat,
-                                 const double* sigma, const int8_t* flow, double* values, int write_cols,
-                                 double* rhs, uint32_t* flags, cudaStream_t st, int mode) {
+cudaError_t launch_assemble_dim2(int P, bool sym, const KArgs& a, const pdg_coeffs& C, cudaStream_t st) {
   switch (P * 2 + (sym ? 1 : 0)) {
-    case 0: return launch_assemble<2, 0, false>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 1: return launch_assemble<2, 0, true>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 2: return launch_assemble<2, 1, false>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 3: return launch_assemble<2, 1, true>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 4: return launch_assemble<2, 2, false>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 5: return launch_assemble<2, 2, true>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 6: return launch_assemble<2, 3, false>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 7: return launch_assemble<2, 3, true>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 8: return launch_assemble<2, 4, false>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 9: return launch_assemble<2, 4, true>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 10: return launch_assemble<2, 5, false>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 11: return launch_assemble<2, 5, true>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 12: return launch_assemble<2, 6, false>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
-    case 13: return launch_assemble<2, 6, true>(m, B, C, R, prm, pat, sigma, flow, values, write_cols, rhs, flags, st, mode);
+    case 0: return launch_assemble<2, 0, false>(a, C, st);
+    case 1: return launch_assemble<2, 0, true>(a, C, st);
+    case 2: return launch_assemble<2, 1, false>(a, C, st);
+    case 3: return launch_assemble<2, 1, true>(a, C, st);
+    case 4: return launch_assemble<2, 2, false>(a, C, st);
+    case 5: return launch_assemble<2, 2, true>(a, C, st);
+    case 6: return launch_assemble<2, 3, false>(a, C, st);
+    case 7: return launch_assemble<2, 3, true>(a, C, st);
+    case 8: return launch_assemble<2, 4, false>(a, C, st);
+    case 9: return launch_assemble<2, 4, true>(a, C, st);
+    case 10: return launch_assemble<2, 5, false>(a, C, st);
+    case 11: return launch_assemble<2, 5, true>(a, C, st);
+    case 12: return launch_assemble<2, 6, false>(a, C, st);
+    case 13: return launch_assemble<2, 6, true>(a, C, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -29,19 +29,10 @@ int num_sms() {
   return sms;
 }
 
-cudaError_t launch_assemble_dim2(int P, bool sym, const pdg_mesh& m, const pdg_basis& B, const pdg_coeffs& C,
-                                 const pdg_rules& R, const pdg_params& prm, const pdg_pattern& pat,
-                                 const double* sigma, const int8_t* flow, double* values, int write_cols,
-                                 double* rhs, uint32_t* flags, cudaStream_t st, int mode);
-cudaError_t launch_assemble_dim3(int P, bool sym, const pdg_mesh& m, const pdg_basis& B, const pdg_coeffs& C,
-                                 const pdg_rules& R, const pdg_params& prm, const pdg_pattern& pat,
-                                 const double* sigma, const int8_t* flow, double* values, int write_cols,
-                                 double* rhs, uint32_t* flags, cudaStream_t st, int mode);
+cudaError_t launch_assemble_dim2(int P, bool sym, const KArgs& a, const pdg_coeffs& C, cudaStream_t st);
+cudaError_t launch_assemble_dim3(int P, bool sym, const KArgs& a, const pdg_coeffs& C, cudaStream_t st);
 
-constexpr int MAX_P_2D = 6;
-constexpr int MAX_P_3D = 4;
-
-static int check_common(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs) {
+int check_common(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs) {
   if (!mesh || !basis || !coeffs) return fail(PDG_ERR_INVALID, "null argument");
   if (mesh->dim != 2 && mesh->dim != 3) return fail(PDG_ERR_UNSUPPORTED, "dim must be 2 or 3");
   const int pmax = mesh->dim == 2 ? MAX_P_2D : MAX_P_3D;
@@ -54,9 +45,32 @@ static int check_common(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_
   return PDG_OK;
 }
 
-static bool symmetric_accumulation(const pdg_coeffs& C) {
+bool symmetric_accumulation(const pdg_coeffs& C) {
   if (C.has_advection) return false;
   return C.diffusion_kind != PDG_DIFF_FULL || C.diffusion_symmetric;
+}
+
+KArgs make_kargs(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_rules* rules, const pdg_params* params,
+                 const pdg_pattern& pat, const pdg_frames* frames, const double* sigma, const int8_t* flow,
+                 double* values, int write_cols, double* rhs, uint32_t* flags, int mode) {
+  KArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.m = *mesh;
+  a.B = *basis;
+  a.R = *rules;
+  a.prm = *params;
+  a.pat = pat;
+  a.sigma = sigma;
+  a.flow = flow;
+  a.sframe = frames->simplex;
+  a.fframe = frames->facet;
+  a.erec = frames->element;
+  a.values = values;
+  a.rhs = rhs;
+  a.flags = flags;
+  a.write_cols = write_cols;
+  a.mode = mode;
+  return a;
 }
 
 // ---- unit kernels -------------------------------------------------------------
@@ -131,50 +145,45 @@ extern "C" const char* pdg_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" int pdg_assemble(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
                             const pdg_rules* rules, const pdg_params* params, const pdg_pattern* pattern,
-                            const double* sigma, const int8_t* face_flow, double* values,
-                            int32_t write_col_idx, double* rhs, uint32_t* err_flags, pdg_stream stream) {
+                            const pdg_frames* frames, const double* sigma, const int8_t* face_flow,
+                            double* values, int32_t write_col_idx, double* rhs, uint32_t* err_flags,
+                            pdg_stream stream) {
   PDG_TRY {
     int rc = check_common(mesh, basis, coeffs);
     if (rc) return rc;
-    if (!rules || !params || !pattern || !sigma || !face_flow || !values || !rhs)
+    if (!rules || !params || !pattern || !frames || !sigma || !face_flow || !values || !rhs)
       return fail(PDG_ERR_INVALID, "null argument");
     if (write_col_idx && !pattern->col_idx) return fail(PDG_ERR_INVALID, "col_idx not allocated");
+    const KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values,
+                               write_col_idx, rhs, err_flags, 0);
     const bool sym = symmetric_accumulation(*coeffs);
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t err =
-        mesh->dim == 2
-            ? launch_assemble_dim2(basis->max_degree, sym, *mesh, *basis, *coeffs, *rules, *params, *pattern,
-                                   sigma, face_flow, values, write_col_idx, rhs, err_flags, st, 0)
-            : launch_assemble_dim3(basis->max_degree, sym, *mesh, *basis, *coeffs, *rules, *params, *pattern,
-                                   sigma, face_flow, values, write_col_idx, rhs, err_flags, st, 0);
-    PDG_CUDA(err);
+    PDG_CUDA(mesh->dim == 2 ? launch_assemble_dim2(basis->max_degree, sym, a, *coeffs, st)
+                            : launch_assemble_dim3(basis->max_degree, sym, a, *coeffs, st));
     return PDG_OK;
   }
   PDG_CATCH
 }
 
 extern "C" int pdg_element_blocks(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
-                                  const pdg_rules* rules, const pdg_params* params, const int32_t* elements,
-                                  int64_t n, double* blocks, double* loads, uint32_t* err_flags,
-                                  pdg_stream stream) {
+                                  const pdg_rules* rules, const pdg_params* params, const pdg_frames* frames,
+                                  const int32_t* elements, int64_t n, double* blocks, double* loads,
+                                  uint32_t* err_flags, pdg_stream stream) {
   PDG_TRY {
     int rc = check_common(mesh, basis, coeffs);
     if (rc) return rc;
-    if (!rules || !params || !elements || !blocks || !loads) return fail(PDG_ERR_INVALID, "null argument");
+    if (!rules || !params || !frames || !elements || !blocks || !loads)
+      return fail(PDG_ERR_INVALID, "null argument");
     pdg_pattern pat;
     std::memset(&pat, 0, sizeof(pat));
     pat.n_row_elements = n;
     pat.row_elements = elements;
-    cudaStream_t st = (cudaStream_t)stream;
-    // dense output: no symmetric mirroring shortcuts are needed, but they are valid
+    const KArgs a = make_kargs(mesh, basis, rules, params, pat, frames, nullptr, nullptr, blocks, 0, loads,
+                               err_flags, 1);
     const bool sym = symmetric_accumulation(*coeffs);
-    cudaError_t err =
-        mesh->dim == 2
-            ? launch_assemble_dim2(basis->max_degree, sym, *mesh, *basis, *coeffs, *rules, *params, pat,
-                                   nullptr, nullptr, blocks, 0, loads, err_flags, st, 1)
-            : launch_assemble_dim3(basis->max_degree, sym, *mesh, *basis, *coeffs, *rules, *params, pat,
-                                   nullptr, nullptr, blocks, 0, loads, err_flags, st, 1);
-    PDG_CUDA(err);
+    cudaStream_t st = (cudaStream_t)stream;
+    PDG_CUDA(mesh->dim == 2 ? launch_assemble_dim2(basis->max_degree, sym, a, *coeffs, st)
+                            : launch_assemble_dim3(basis->max_degree, sym, a, *coeffs, st));
     return PDG_OK;
   }
   PDG_CATCH

@@ -28,6 +28,11 @@ int fail(int code, const std::string& msg);
 
 int num_sms();
 
+constexpr int MAX_P_2D = 6;
+constexpr int MAX_P_3D = 4;
+int check_common(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs);
+bool symmetric_accumulation(const pdg_coeffs& C);
+
 // launch accounting (pdg_launch_count): every kernel launch site calls this
 void note_launch();
 
@@ -45,22 +50,24 @@ inline int grid_for_warps(int64_t nwarps, int threads) {
 
 cudaError_t exclusive_scan(const int64_t* in, int64_t n, int64_t* out, int64_t* ws, cudaStream_t st);
 
-// col_idx of all rows of element e: row a, position c -> the c-th column of
-// the concatenated neighbour DoF ranges (assembly.py:319-324).
+// col_idx of all rows of element e (assembly.py:319-324): lanes over column
+// positions, each resolved by a short walk of the sorted neighbour list
+// (division free), then stored down the element's rows.
 __device__ __forceinline__ void write_col_rows(const pdg_basis& B, const pdg_pattern& P, int32_t e,
                                                int64_t val_off, int64_t L, int lane) {
   const int64_t ne = B.dof_offset[e + 1] - B.dof_offset[e];
-  int64_t colstart = 0;
-  for (int64_t q = P.nbr_ptr[e]; q < P.nbr_ptr[e + 1]; ++q) {
-    const int32_t j = P.nbr_elem[q];
-    const int64_t d0 = B.dof_offset[j];
-    const int64_t nj = B.dof_offset[j + 1] - d0;
-    const int64_t tot = ne * nj;
-    for (int64_t idx = lane; idx < tot; idx += 32) {
-      const int64_t a = idx / nj, c = idx - a * nj;
-      P.col_idx[val_off + a * L + colstart + c] = d0 + c;
+  const int64_t q0 = P.nbr_ptr[e], q1 = P.nbr_ptr[e + 1];
+  for (int64_t p = lane; p < L; p += 32) {
+    int64_t cs = 0, q = q0, d0 = 0;
+    for (; q < q1; ++q) {
+      const int32_t j = P.nbr_elem[q];
+      d0 = B.dof_offset[j];
+      const int64_t nj = B.dof_offset[j + 1] - d0;
+      if (p < cs + nj) break;
+      cs += nj;
     }
-    colstart += nj;
+    const int64_t cv = d0 + (p - cs);
+    for (int64_t r = 0; r < ne; ++r) P.col_idx[val_off + r * L + p] = cv;
   }
 }
 

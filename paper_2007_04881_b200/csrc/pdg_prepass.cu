@@ -243,3 +243,70 @@ extern "C" int pdg_face_prepass(const pdg_mesh* mesh, const pdg_basis* basis, co
   }
   PDG_CATCH
 }
+
+// ---------------------------------------------------------------------------
+// geometry pre-pass: affine frames of every simplex (element order), every
+// facet, and the basis constants of every element
+// ---------------------------------------------------------------------------
+namespace pdg {
+
+template <int DIM>
+__global__ void frames_kernel(const pdg_mesh m, const pdg_basis B, const pdg_frames F, uint32_t* flags) {
+  constexpr int W = DIM == 2 ? 8 : 16;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = tid; i < m.n_simplices; i += stride) {
+    double v0[3], E[3][3];
+    const double det = simplex_frame<DIM>(m, m.elem_simplices[i], v0, E, flags);
+    double* o = F.simplex + i * W;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) o[d] = v0[d];
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
+    o[DIM + DIM * DIM] = det;
+  }
+  for (int64_t r = tid; r < m.n_facets; r += stride) {
+    double v0[3], E[3][3];
+    const double jac = facet_frame<DIM>(m, r, v0, E, flags);
+    double* o = F.facet + r * W;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) o[d] = v0[d];
+#pragma unroll
+    for (int k = 0; k < DIM - 1; ++k)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
+    o[DIM + (DIM - 1) * DIM] = jac;
+  }
+  for (int64_t e = tid; e < m.n_elements; e += stride) {
+    const BoxConst<DIM> b = box_const<DIM>(B.box + e * 2 * DIM);
+    double* o = F.element + e * W;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      o[d] = b.c[d];
+      o[DIM + d] = b.ih[d];
+      o[2 * DIM + d] = b.rs[d];
+    }
+  }
+}
+
+}  // namespace pdg
+
+extern "C" int pdg_frames_build(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_frames* frames,
+                                uint32_t* err_flags, pdg_stream stream) {
+  PDG_TRY {
+    if (!mesh || !basis || !frames || !frames->simplex || !frames->facet || !frames->element)
+      return fail(PDG_ERR_INVALID, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = std::max(mesh->n_simplices, std::max(mesh->n_facets, mesh->n_elements));
+    if (n == 0) return PDG_OK;
+    if (mesh->dim == 2) frames_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(*mesh, *basis, *frames, err_flags);
+    else if (mesh->dim == 3) frames_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(*mesh, *basis, *frames, err_flags);
+    else return fail(PDG_ERR_UNSUPPORTED, "dim must be 2 or 3");
+    note_launch();
+    PDG_CUDA(cudaGetLastError());
+    return PDG_OK;
+  }
+  PDG_CATCH
+}

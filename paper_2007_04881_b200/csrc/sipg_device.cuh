@@ -13,10 +13,14 @@
 // registers per thread, leaving issue slots and registers for the rest.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 #include "../../include/pdg.h"
+
+#define PDG_INF __longlong_as_double(0x7ff0000000000000LL)
 
 namespace pdg {
 

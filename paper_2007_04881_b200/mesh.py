@@ -241,6 +241,11 @@ class FlatMesh:
         iptr = np.zeros(len(ifs) + 1, np.int64)
         np.cumsum([len(i.face_ids) for i in ifs], out=iptr[1:])
         ifaces = cat([np.asarray(i.face_ids, np.int64) for i in ifs], np.int32, (0,))
+        if not np.array_equal(ifaces, np.arange(ifaces.size)):
+            # polydg emits the faces of each interface consecutively, interfaces
+            # in sorted order, before all boundary faces (mesh.py:451-455); the
+            # kernels address an interface's faces as the id range iface_ptr.
+            raise NotImplementedError("interface faces must be the contiguous leading face ids")
         bfaces = np.flatnonzero(nbr == BOUNDARY)
         bowner = owner[bfaces]
         order = np.argsort(bowner, kind="stable")

@@ -469,3 +469,77 @@ def compile_coeffs(coeffs, dim: int) -> dict:
         raise NotImplementedError("coefficient programs exceed the device program capacity")
     desc["code"], desc["consts"] = code, consts
     return desc
+
+
+# ---------------------------------------------------------------------------
+# runtime-specialised policy (CUDA source for pdg_assemble_jit)
+# ---------------------------------------------------------------------------
+
+_CFN = {OP_SIN: "sin", OP_COS: "cos", OP_EXP: "exp", OP_LOG: "log", OP_SQRT: "sqrt",
+        OP_ABS: "fabs", OP_TANH: "tanh"}
+_COP = {OP_ADD: "+", OP_SUB: "-", OP_MUL: "*", OP_DIV: "/"}
+
+
+def cuda_expr(e: Expr) -> str:
+    """C expression with the same operation order as the numpy evaluation."""
+    if e.op == OP_CONST:
+        v = float(e.value)
+        if not np.isfinite(v):
+            raise NotImplementedError("non-finite constant in a coefficient")
+        return f"({v!r})"
+    if e.op == OP_COORD:
+        return f"x[{int(e.value)}]"
+    if e.op in _COP:
+        return f"({cuda_expr(e.args[0])} {_COP[e.op]} {cuda_expr(e.args[1])})"
+    if e.op == OP_POW:
+        base, ex = e.args
+        if ex.op == OP_CONST and float(ex.value) == 2.0:  # numpy squares exactly
+            b = cuda_expr(base)
+            return f"({b} * {b})"
+        return f"pow({cuda_expr(base)}, {cuda_expr(ex)})"
+    if e.op == OP_NEG:
+        return f"(-{cuda_expr(e.args[0])})"
+    return f"{_CFN[e.op]}({cuda_expr(e.args[0])})"
+
+
+def policy_source(coeffs, dim: int) -> str:
+    """CUDA source of the coefficient policy class ``JitCoef`` consumed by
+    ``assemble_body`` (csrc/assemble_body.cuh, see InterpCoef for the
+    interface)."""
+    ten = as_tensor(coeffs.diffusion, dim, "diffusion")
+    kind, ent = 0, None
+    if ten is not None:
+        k, val = ten
+        if k == "full" and all(e.is_constant for e in val):
+            m = np.array([e.value for e in val]).reshape(dim, dim)
+            if np.all(m == np.diag(np.diag(m))) and np.all(np.diag(m) == m[0, 0]):
+                k, val = "iso", const(m[0, 0])
+        kind, ent = (1, val) if k == "iso" else (2, val)
+    adv = as_vector_exprs(coeffs.advection, dim, "advection")
+    sc = {n: as_scalar_expr(getattr(coeffs, f), f) for n, f in
+          (("c", "reaction"), ("f", "source"), ("gD", "dirichlet_data"), ("gN", "neumann_data"))}
+    b = lambda v: "true" if v else "false"
+    out = ["struct JitCoef {",
+           f"  __device__ static constexpr int diff_kind() {{ return {kind}; }}",
+           f"  __device__ static constexpr bool has_adv() {{ return {b(adv is not None)}; }}",
+           f"  __device__ static constexpr bool has_reac() {{ return {b(sc['c'] is not None)}; }}",
+           f"  __device__ static constexpr bool has_src() {{ return {b(sc['f'] is not None)}; }}",
+           f"  __device__ static constexpr bool has_dir() {{ return {b(sc['gD'] is not None)}; }}",
+           f"  __device__ static constexpr bool has_neu() {{ return {b(sc['gN'] is not None)}; }}"]
+    iso = cuda_expr(ent) if kind == 1 else "1.0"
+    out.append(f"  __device__ double a_iso(const double* x) const {{ return {iso}; }}")
+    cases = ""
+    if kind == 2:
+        cases = " ".join(f"case {k}: return {cuda_expr(e)};" for k, e in enumerate(ent))
+    out.append(f"  __device__ double a_ij(int i, int j, const double* x) const "
+               f"{{ switch (i * {dim} + j) {{ {cases} default: break; }} return 0.0; }}")
+    cases = ""
+    if adv is not None:
+        cases = " ".join(f"case {k}: return {cuda_expr(e)};" for k, e in enumerate(adv))
+    out.append(f"  __device__ double b_i(int i, const double* x) const "
+               f"{{ switch (i) {{ {cases} default: break; }} return 0.0; }}")
+    for n in ("c", "f", "gD", "gN"):
+        body = cuda_expr(sc[n]) if sc[n] is not None else "0.0"
+        out.append(f"  __device__ double {n}(const double* x) const {{ return {body}; }}")
+    out.append("};")
+    return "\n".join(out)
