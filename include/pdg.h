@@ -178,6 +178,7 @@ typedef struct pdg_frames {
   double* element;
 } pdg_frames;
 
+#ifndef __CUDACC_RTC__ /* the runtime-compiled kernels need the types only */
 int pdg_abi_version(void);
 const char* pdg_last_error(void);
 
@@ -270,6 +271,8 @@ int pdg_element_blocks(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_c
                        const pdg_rules* rules, const pdg_params* params, const pdg_frames* frames,
                        const int32_t* elements, int64_t n, double* blocks, double* loads,
                        uint32_t* err_flags, pdg_stream stream);
+
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -153,7 +153,7 @@ static std::string get_kernel(const std::string& policy, int dim, int P, bool sy
   const std::string dir = lib_dir();
   const std::string src = full_source(policy, dim, P, sym);
   std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
-                                   "--expt-relaxed-constexpr", "-I" + dir + "/csrc",
+                                   "-I" + dir + "/csrc",
                                    "-I" + dir + "/../include"};
   std::string key = src;
   for (auto& o : opts) key += "\n" + o;

@@ -85,7 +85,7 @@ template <int DIM, int P>
 struct MultiIdx {
   static constexpr int NB = binom(P + DIM, DIM);
   int a[NB][3];
-  constexpr MultiIdx() : a{} {
+  __host__ __device__ constexpr MultiIdx() : a{} {
     int f = 0;
     for (int tot = 0; tot <= P; ++tot) {
       if (DIM == 2) {
