@@ -39,9 +39,17 @@
 
 namespace pdg {
 
+// RHS partials of a lane live in registers when the basis has at most this
+// many functions, else in a lane-private shared-memory column (fewer
+// registers, more shared memory); the runtime specialisation sets it per
+// compile (pdg_jit.cu), the host layout (make_layout) must agree.
+#ifndef PDG_RHS_REGS_MAX
+#define PDG_RHS_REGS_MAX 20
+#endif
+
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
-constexpr int NBR_WIN = 32;  // neighbour entries staged per window
+constexpr int NBR_WIN = 16;  // neighbour entries staged per window
 
 template <int DIM>
 struct Widths {
@@ -81,12 +89,16 @@ struct Shape {
   static constexpr int NB = binom(P + DIM, DIM);
   static constexpr int NT = (NB + 7) / 8;
   static constexpr int NBP = NT * 8;
-  static constexpr bool RHS_REGS = NB <= 20;
+  static constexpr bool RHS_REGS = NB <= PDG_RHS_REGS_MAX;
 };
 
-// per-warp staging of the neighbour window (ints) -- after the scalars
+// per-warp staging of the neighbour window -- after the scalars
 struct NbrStage {
+  double sig[NBR_WIN];     // penalty of the interface's first face
+  double nrm[3][NBR_WIN];  // its owner normal
   int j[NBR_WIN], nj[NBR_WIN], col[NBR_WIN], fa[NBR_WIN], fb[NBR_WIN], pj[NBR_WIN];
+  int info[NBR_WIN];       // bit0 e is the neighbour side, bit1 e downwind, bit2 paired-round eligible
+  int row0[NBR_WIN];       // first sub-facet row of the first face
 };
 
 // Ahead-of-time coefficient policy: interprets the bytecode in pdg_coeffs.
@@ -108,6 +120,10 @@ struct InterpCoef {
   __device__ double gD(const double* x) const { return eval_prog(C, C.dirichlet, x); }
   __device__ double gN(const double* x) const { return eval_prog(C, C.neumann, x); }
 };
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 template <int DIM>
 __device__ __forceinline__ BoxConst<DIM> load_box(const double* erec, int64_t e) {
@@ -348,25 +364,147 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       }
     }
 
+    // warm L2 with the next element's simplex frames while the face phase runs
+    {
+      const int64_t kn = k + nwarps;
+      if (kn < pat.n_row_elements) {
+        const int32_t en = pat.row_elements ? pat.row_elements[kn] : (int32_t)kn;
+        const int64_t s0n = m.elem_ptr[en], s1n = m.elem_ptr[en + 1];
+        const char* p0 = reinterpret_cast<const char*>(a.sframe + s0n * W::SF);
+        const int64_t bytes = (s1n - s0n) * W::SF * 8;
+        for (int64_t off = (int64_t)lane * 128; off < bytes; off += 32 * 128) prefetch_l2(p0 + off);
+        if (lane == 0) prefetch_l2(a.erec + (int64_t)en * W::ER);
+      }
+    }
+
     // ------------------------------------------------------------ interfaces
+    // Neighbour entries are staged NBR_WIN at a time (lane = entry): element,
+    // DoF count, column start, face range and the first face's metadata, so
+    // the face loop below reads shared memory instead of chains of dependent
+    // global loads.  Two interfaces made of a single sub-facet with <= 8
+    // quadrature points (every 2D Voronoi interface up to p = 6) share one
+    // tabulation round: slots 0-7 / 8-15, own trace on lanes 0-15, the
+    // neighbour's on lanes 16-31.
     int64_t colself = 0;
     const int64_t q0 = mode ? 0 : pat.nbr_ptr[e];
     const int nnb = mode ? 0 : (int)(pat.nbr_ptr[e + 1] - q0);
     int colcarry = 0;
+    const bool mine = lane < KF;
+    const int slot = lane & (KF - 1);
+
+    // tabulate one face slot: own trace (lanes 0-15) or neighbour trace (16-31)
+    auto tab_slot = [&](const double* nrm, int64_t frow, int r0, int kq, double valid, double sig, double sgn,
+                        bool down, const BoxConst<DIM>& bo) {
+      const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+      double x[3] = {0.0, 0.0, 0.0};
+      const double jac = frame_point<DIM, DIM - 1>(a.fframe + frow * W::FF, xi, x);
+      const double w = R.weights[r0 + kq] * jac * valid;
+      Tab<DIM, P> tb;
+      tb.load(mine ? bx : bo, x);
+      double av = 1.0;
+      double A[DIM][DIM];
+      if (grad_terms) {
+        if (full) {
+#pragma unroll
+          for (int i = 0; i < DIM; ++i)
+#pragma unroll
+            for (int jj = 0; jj < DIM; ++jj) A[i][jj] = cf.a_ij(i, jj, x);
+        } else {
+          av = cf.a_iso(x);
+        }
+      }
+      double* col = buf + slot;
+      const int rv = mine ? 0 : 2;
+      const double vs = mine ? 1.0 : -1.0;
+#pragma unroll
+      for (int ff = 0; ff < NBP; ++ff) {
+        double vv = 0.0, fl = 0.0;
+        if (ff < NB) {
+          vv = tb.val(ff);
+          if (grad_terms) fl = face_flux<DIM, P>(cf, tb, ff, nrm, av, A);
+        }
+        col[(rv * NBP + ff) * KFP] = vs * vv;
+        col[((rv + 1) * NBP + ff) * KFP] = fl;
+      }
+      if (mine) {
+        double wbn = 0.0;
+        if (down) {
+          double bn = 0.0;
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) bn += cf.b_i(i, x) * nrm[i];
+          wbn = w * bn;
+        }
+        sc1[slot] = w * sig - sgn * wbn;
+        sc2[slot] = grad_terms ? -0.5 * sgn * w : 0.0;
+      }
+    };
+    // contract k-steps [k0, k1) of the face table into the diagonal tiles and co
+    auto face_contract = [&](int k0, int k1, double (&co)[NT][NT][2]) {
+      for (int kk = k0; kk < k1; ++kk) {
+        const int qq = kk * 4 + t;
+        const double al = sc1[qq], be = sc2[qq];
+        double va[NT], fa[NT], nvb[NT], fb[NT], l1[NT], l2[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          va[i] = buf[(0 * NBP + i * 8 + g) * KFP + qq];
+          nvb[i] = buf[(2 * NBP + i * 8 + g) * KFP + qq];
+          if (grad_terms) {
+            fa[i] = buf[(1 * NBP + i * 8 + g) * KFP + qq];
+            fb[i] = buf[(3 * NBP + i * 8 + g) * KFP + qq];
+            l1[i] = al * va[i] + be * fa[i];
+            l2[i] = be * va[i];
+          } else {
+            fa[i] = fb[i] = l2[i] = 0.0;
+            l1[i] = al * va[i];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < NT; ++r)
+#pragma unroll
+          for (int cc = 0; cc < NT; ++cc) {
+            if (!SYM || cc >= r) {
+              dmma(cd[r][cc], l1[r], va[cc]);
+              if (grad_terms) dmma(cd[r][cc], l2[r], fa[cc]);
+            }
+            dmma(co[r][cc], l1[r], nvb[cc]);
+            if (grad_terms) dmma(co[r][cc], l2[r], fb[cc]);
+          }
+      }
+    };
+
     for (int w0 = 0; w0 < nnb; w0 += NBR_WIN) {
       const int nw = min(NBR_WIN, nnb - w0);
-      // stage the window: neighbour, its DoF count, column start, face range
       {
         int nj = 0;
+        bool is_self = false;
         if (lane < nw) {
           const int32_t j = pat.nbr_elem[q0 + w0 + lane];
           const int32_t ifc = pat.nbr_iface[q0 + w0 + lane];
           nj = (int)(B.dof_offset[j + 1] - B.dof_offset[j]);
+          is_self = j == e;
           ns->j[lane] = j;
           ns->nj[lane] = nj;
-          ns->pj[lane] = B.degree[j];
-          ns->fa[lane] = ifc >= 0 ? (int)m.iface_ptr[ifc] : 0;
-          ns->fb[lane] = ifc >= 0 ? (int)m.iface_ptr[ifc + 1] : 0;
+          const int pj = B.degree[j];
+          ns->pj[lane] = pj;
+          int fa = 0, fb = 0, info = 0, row0 = 0, nrows = 0;
+          if (!is_self) {
+            fa = (int)m.iface_ptr[ifc];
+            fb = (int)m.iface_ptr[ifc + 1];
+            const int side = m.face_owner[fa] == e ? 0 : 1;
+            const bool down = cf.has_adv() && a.flow[fa] == side;
+            row0 = (int)m.face_ptr[fa];
+            nrows = (int)(m.face_ptr[fa + 1] - row0);
+            const int nq = R.face_count[2 * max(pe, pj) + a.prm.quad_increment];
+            const bool simple = fb - fa == 1 && nrows == 1 && nq <= 8;
+            info = side | (down ? 2 : 0) | (simple ? 4 : 0);
+            ns->sig[lane] = a.sigma[fa];
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) ns->nrm[i][lane] = m.face_normal[(int64_t)fa * DIM + i];
+          }
+          ns->fa[lane] = fa;
+          ns->fb[lane] = fb;
+          ns->info[lane] = info;
+          ns->row0[lane] = row0;
         }
         int incl = nj;
 #pragma unroll
@@ -376,133 +514,101 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         }
         if (lane < nw) ns->col[lane] = colcarry + incl - nj;
         colcarry += __shfl_sync(0xffffffffu, incl, 31);
+        const unsigned selfm = __ballot_sync(0xffffffffu, is_self);
+        __syncwarp();
+        if (selfm) colself = ns->col[__ffs(selfm) - 1];
       }
       __syncwarp();
       // col_idx of this window's column span, all rows (division-free)
       if (a.write_cols) {
         const int c0 = ns->col[0];
         const int c1 = ns->col[nw - 1] + ns->nj[nw - 1];
+        int q = 0;
         for (int p = c0 + lane; p < c1; p += 32) {
-          int q = 0;
           while (q + 1 < nw && ns->col[q + 1] <= p) ++q;
           const int64_t cv = B.dof_offset[ns->j[q]] + (p - ns->col[q]);
           int64_t* dst = pat.col_idx + voff + p;
           for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
         }
       }
-      for (int qi = 0; qi < nw; ++qi) {
-        const int32_t j = ns->j[qi];
-        const int nj = ns->nj[qi];
-        const int colstart = ns->col[qi];
-        if (j == e) {
-          colself = colstart;
+      int qi = 0;
+      while (qi < nw) {
+        if (ns->j[qi] == e) {
+          ++qi;
           continue;
         }
-        const BoxConst<DIM> bo = load_box<DIM>(a.erec, j);
-        const int pj = ns->pj[qi];
+        int qb = qi + 1;
+        if (qb < nw && ns->j[qb] == e) ++qb;
+        const bool pair = (ns->info[qi] & 4) && qb < nw && (ns->info[qb] & 4);
         double co[NT][NT][2];
         zero_tiles<NT>(co);
-        const int fend = ns->fb[qi];
-        for (int f = ns->fa[qi]; f < fend; ++f) {
-          const int side = m.face_owner[f] == e ? 0 : 1;
-          const double sgn = side == 0 ? 1.0 : -1.0;
-          const double sig = a.sigma[f];
-          const bool down = cf.has_adv() && a.flow[f] == side;
+        if (pair) {
+          // ---- two single-facet interfaces in one round
+          const int seg = slot >> 3, ls = slot & 7;
+          const int q = seg ? qb : qi;
+          const int info = ns->info[q];
+          const int pj = ns->pj[q];
           const int order = 2 * max(pe, pj) + a.prm.quad_increment;
           const int r0 = R.face_offset[order], nq = R.face_count[order];
           double nrm[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-          for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)f * DIM + i];
-          const int64_t row0 = m.face_ptr[f];
-          const int Pf = (int)(m.face_ptr[f + 1] - row0) * nq;
-          const bool mine = lane < KF;
-          const int slot = lane & (KF - 1);
+          for (int i = 0; i < DIM; ++i) nrm[i] = ns->nrm[i][q];
+          const BoxConst<DIM> bo = load_box<DIM>(a.erec, ns->j[q]);
+          tab_slot(nrm, ns->row0[q], r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, ns->sig[q],
+                   (info & 1) ? -1.0 : 1.0, (info & 2) != 0, bo);
+          __syncwarp();
+          face_contract(0, 2, co);
+          store_block<NT, false>(a.values, voff, Lrow, ns->col[qi], ne, ns->nj[qi], co, g, t);
+          zero_tiles<NT>(co);
+          face_contract(2, 4, co);
+          store_block<NT, false>(a.values, voff, Lrow, ns->col[qb], ne, ns->nj[qb], co, g, t);
+          __syncwarp();
+          qi = qb + 1;
+          continue;
+        }
+        // ---- general interface: every face, every sub-facet, rounds of 16 points
+        const int32_t j = ns->j[qi];
+        const int pj = ns->pj[qi];
+        const BoxConst<DIM> bo = load_box<DIM>(a.erec, j);
+        const int order = 2 * max(pe, pj) + a.prm.quad_increment;
+        const int r0 = R.face_offset[order], nq = R.face_count[order];
+        const int fend = ns->fb[qi];
+        for (int f = ns->fa[qi]; f < fend; ++f) {
+          int side, info;
+          double sig;
+          double nrm[3] = {0.0, 0.0, 0.0};
+          int64_t row0;
+          int nrows;
+          if (f == ns->fa[qi]) {
+            info = ns->info[qi];
+            side = info & 1;
+            sig = ns->sig[qi];
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) nrm[i] = ns->nrm[i][qi];
+            row0 = ns->row0[qi];
+          } else {
+            side = m.face_owner[f] == e ? 0 : 1;
+            info = side | ((cf.has_adv() && a.flow[f] == side) ? 2 : 0);
+            sig = a.sigma[f];
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)f * DIM + i];
+            row0 = m.face_ptr[f];
+          }
+          nrows = (int)(m.face_ptr[f + 1] - row0);
+          const int Pf = nrows * nq;
           for (int base = 0; base < Pf; base += KF) {
             const int nvalid = min(KF, Pf - base);
-            {
-              const int gq = base + min(slot, nvalid - 1);
-              const double valid = slot < nvalid ? 1.0 : 0.0;
-              const int lr = gq / nq;
-              const int kq = gq - lr * nq;
-              const double* xi = R.points + (int64_t)(r0 + kq) * 3;
-              double x[3] = {0.0, 0.0, 0.0};
-              const double jac = frame_point<DIM, DIM - 1>(a.fframe + (row0 + lr) * W::FF, xi, x);
-              const double w = R.weights[r0 + kq] * jac * valid;
-              Tab<DIM, P> tb;
-              tb.load(mine ? bx : bo, x);
-              double av = 1.0;
-              double A[DIM][DIM];
-              if (grad_terms) {
-                if (full) {
-#pragma unroll
-                  for (int i = 0; i < DIM; ++i)
-#pragma unroll
-                    for (int jj = 0; jj < DIM; ++jj) A[i][jj] = cf.a_ij(i, jj, x);
-                } else {
-                  av = cf.a_iso(x);
-                }
-              }
-              double* col = buf + slot;
-              const int rv = mine ? 0 : 2;
-              const double vs = mine ? 1.0 : -1.0;
-#pragma unroll
-              for (int ff = 0; ff < NBP; ++ff) {
-                double vv = 0.0, fl = 0.0;
-                if (ff < NB) {
-                  vv = tb.val(ff);
-                  if (grad_terms) fl = face_flux<DIM, P>(cf, tb, ff, nrm, av, A);
-                }
-                col[(rv * NBP + ff) * KFP] = vs * vv;
-                col[((rv + 1) * NBP + ff) * KFP] = fl;
-              }
-              if (mine) {
-                double wbn = 0.0;
-                if (down) {
-                  double bn = 0.0;
-#pragma unroll
-                  for (int i = 0; i < DIM; ++i) bn += cf.b_i(i, x) * nrm[i];
-                  wbn = w * bn;
-                }
-                sc1[slot] = w * sig - sgn * wbn;
-                sc2[slot] = grad_terms ? -0.5 * sgn * w : 0.0;
-              }
-            }
+            const int gq = base + min(slot, nvalid - 1);
+            const int lr = gq / nq;
+            tab_slot(nrm, row0 + lr, r0, gq - lr * nq, slot < nvalid ? 1.0 : 0.0, sig, side ? -1.0 : 1.0,
+                     (info & 2) != 0, bo);
             __syncwarp();
-            const int nk = (nvalid + 3) >> 2;
-            for (int kk = 0; kk < nk; ++kk) {
-              const int qq = kk * 4 + t;
-              const double al = sc1[qq], be = sc2[qq];
-              double va[NT], fa[NT], nvb[NT], fb[NT], l1[NT], l2[NT];
-#pragma unroll
-              for (int i = 0; i < NT; ++i) {
-                va[i] = buf[(0 * NBP + i * 8 + g) * KFP + qq];
-                nvb[i] = buf[(2 * NBP + i * 8 + g) * KFP + qq];
-                if (grad_terms) {
-                  fa[i] = buf[(1 * NBP + i * 8 + g) * KFP + qq];
-                  fb[i] = buf[(3 * NBP + i * 8 + g) * KFP + qq];
-                  l1[i] = al * va[i] + be * fa[i];
-                  l2[i] = be * va[i];
-                } else {
-                  fa[i] = fb[i] = l2[i] = 0.0;
-                  l1[i] = al * va[i];
-                }
-              }
-#pragma unroll
-              for (int r = 0; r < NT; ++r)
-#pragma unroll
-                for (int cc = 0; cc < NT; ++cc) {
-                  if (!SYM || cc >= r) {
-                    dmma(cd[r][cc], l1[r], va[cc]);
-                    if (grad_terms) dmma(cd[r][cc], l2[r], fa[cc]);
-                  }
-                  dmma(co[r][cc], l1[r], nvb[cc]);
-                  if (grad_terms) dmma(co[r][cc], l2[r], fb[cc]);
-                }
-            }
+            face_contract(0, (nvalid + 3) >> 2, co);
             __syncwarp();
           }
         }
-        store_block<NT, false>(a.values, voff, Lrow, colstart, ne, nj, co, g, t);
+        store_block<NT, false>(a.values, voff, Lrow, ns->col[qi], ne, ns->nj[qi], co, g, t);
+        ++qi;
       }
       __syncwarp();
     }

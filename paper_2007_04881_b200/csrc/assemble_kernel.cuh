@@ -11,10 +11,10 @@ namespace pdg {
 // Per-warp shared-memory plan of the element kernel (must mirror the carving
 // at the top of assemble_body): volume / face tables, 64 scalars, the
 // neighbour staging window, and lane-private RHS partials for large bases.
-inline AsmLayout make_layout(int dim, int P, int diff_kind, bool has_vr) {
+inline AsmLayout make_layout(int dim, int P, int diff_kind, bool has_vr, int rhs_regs_max = PDG_RHS_REGS_MAX) {
   const int NB = binom(P + dim, dim);
   const int NBP = ((NB + 7) / 8) * 8;
-  const bool rhs_regs = NB <= 20;
+  const bool rhs_regs = NB <= rhs_regs_max;
   AsmLayout L;
   const int nG = diff_kind != PDG_DIFF_NONE ? dim : 0;
   const int nAG = diff_kind == PDG_DIFF_FULL ? dim : 0;

@@ -121,6 +121,12 @@ struct JitKernel {
 static std::mutex g_mu;
 static std::unordered_map<std::string, JitKernel> g_cache;
 
+// PDG_RHS_REGS_MAX for runtime compiles (env override for experiments)
+static int jit_rhs_regs_max() {
+  const char* v = getenv("PDG_RHS_REGS_MAX");
+  return v ? atoi(v) : PDG_RHS_REGS_MAX;
+}
+
 static std::string full_source(const std::string& policy, int dim, int P, bool sym) {
   // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow
   // (register cap = 64K / (128 * n)); default 4 = 128 registers, 16 warps/SM
@@ -154,6 +160,7 @@ static std::string get_kernel(const std::string& policy, int dim, int P, bool sy
   const std::string dir = lib_dir();
   const std::string src = full_source(policy, dim, P, sym);
   std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                                   "-DPDG_RHS_REGS_MAX=" + std::to_string(jit_rhs_regs_max()),
                                    "-I" + dir + "/csrc",
                                    "-I" + dir + "/../include"};
   std::string key = src;
@@ -263,7 +270,7 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values, write_col_idx,
                          rhs, err_flags, 0);
     a.lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind,
-                        coeffs->has_advection || coeffs->has_reaction);
+                        coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max());
     const int threads = 128;
     const size_t smem = (size_t)a.lay.warp_doubles * 8 * (threads / 32);
     Api& A = api();

@@ -543,3 +543,42 @@ def policy_source(coeffs, dim: int) -> str:
         out.append(f"  __device__ double {n}(const double* x) const {{ return {body}; }}")
     out.append("};")
     return "\n".join(out)
+
+
+def _pi_multiple(v: float):
+    """k if v == k * float(pi) exactly for a small integer k, else None."""
+    k = round(v / math.pi)
+    if k != 0 and abs(k) <= 64 and float(k) * math.pi == v:
+        return int(k)
+    return None
+
+
+_cuda_expr_plain = cuda_expr
+
+
+def cuda_expr(e: Expr) -> str:  # noqa: F811  (extends the plain lowering)
+    """As the plain lowering, with sin/cos of (k*pi)*u emitted as sinpi/cospi(k*u):
+    the same value up to the rounding of k*pi*u (<= 1 ulp of the argument),
+    without the pi/2 argument reduction of sin/cos."""
+    if e.op in (OP_SIN, OP_COS) and e.args[0].op == OP_MUL:
+        a, b = e.args[0].args
+        for c, u in ((a, b), (b, a)):
+            if c.op == OP_CONST:
+                k = _pi_multiple(float(c.value))
+                if k is not None:
+                    fn = "sinpi" if e.op == OP_SIN else "cospi"
+                    arg = cuda_expr(u) if k == 1 else f"({float(k)!r} * {cuda_expr(u)})"
+                    return f"{fn}({arg})"
+    if e.op in _COP:
+        return f"({cuda_expr(e.args[0])} {_COP[e.op]} {cuda_expr(e.args[1])})"
+    if e.op == OP_POW:
+        base, ex = e.args
+        if ex.op == OP_CONST and float(ex.value) == 2.0:
+            b = cuda_expr(base)
+            return f"({b} * {b})"
+        return f"pow({cuda_expr(base)}, {cuda_expr(ex)})"
+    if e.op == OP_NEG:
+        return f"(-{cuda_expr(e.args[0])})"
+    if e.op in _CFN:
+        return f"{_CFN[e.op]}({cuda_expr(e.args[0])})"
+    return _cuda_expr_plain(e)

@@ -22,7 +22,7 @@ def main(cfg="cfg5", degree=None, sym=True, minblocks=2):
     prog = C.c_void_p()
     assert lib.nvrtcCreateProgram(C.byref(prog), src.encode(), b"pdg_jit.cu", 0, None, None) == 0
     d = os.path.join(ROOT, "paper_2007_04881_b200")
-    opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo",
+    opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", f"-DPDG_RHS_REGS_MAX={os.environ.get('PDG_RHS_REGS_MAX', 20)}".encode(),
             f"-I{d}/csrc".encode(), f"-I{d}/../include".encode(), b"-Xptxas=-v"]
     arr = (C.c_char_p * len(opts))(*opts)
     rc = lib.nvrtcCompileProgram(prog, len(opts), arr)
