@@ -129,10 +129,10 @@ static int jit_rhs_regs_max() {
 
 static std::string full_source(const std::string& policy, int dim, int P, bool sym) {
   // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow
-  // (register cap = 64K / (128 * n)); default 4 = 128 registers, 16 warps/SM
-  // (measured: 2 -> 11.0 ms, 3 -> 9.2 ms, 4 -> 8.95 ms on 400k cfg5 cells)
+  // (register cap = 64K / (128 * n)); default 3 = 168 registers, 12 warps/SM
+  // (v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells)
   const char* mb = getenv("PDG_JIT_MINBLOCKS");
-  const int minblocks = mb ? std::max(1, atoi(mb)) : 4;
+  const int minblocks = mb ? std::max(1, atoi(mb)) : 3;
   std::ostringstream os;
   os << "#include \"assemble_body.cuh\"\n"
      << "namespace pdg_jit {\nusing namespace pdg;\n"

@@ -65,6 +65,9 @@ class Expr:
             return np.full(pts.shape[0], self.value)
         if self.op == OP_COORD:
             return pts[:, int(self.value)]
+        if self.op == OP_POW and self.args[1].op == OP_CONST:
+            # scalar exponent: numpy's fast paths (x**2 -> square), as user code would
+            return self.args[0]._eval(pts) ** float(self.args[1].value)
         if self.op in _BINARY:
             return _BINARY[self.op](self.args[0]._eval(pts), self.args[1]._eval(pts))
         return _UNARY[self.op](self.args[0]._eval(pts))
