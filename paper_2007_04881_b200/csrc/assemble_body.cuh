@@ -47,6 +47,16 @@ namespace pdg {
 #define PDG_RHS_REGS_MAX 20
 #endif
 
+// unroll factors of the k-step loops (tuning knobs, PDG_JIT_DEFINES)
+#define PDG_STR_(x) #x
+#define PDG_UNROLL(n) _Pragma(PDG_STR_(unroll n))
+#ifndef PDG_VOL_UNROLL
+#define PDG_VOL_UNROLL 1
+#endif
+#ifndef PDG_FACE_UNROLL
+#define PDG_FACE_UNROLL 1
+#endif
+
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
 constexpr int NBR_WIN = 16;  // neighbour entries staged per window
@@ -325,6 +335,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         }
         __syncwarp();
         const int nk = (nvalid + 3) >> 2;
+        PDG_UNROLL(PDG_VOL_UNROLL)
         for (int kk = 0; kk < nk; ++kk) {
           const int q = kk * 4 + t;
           if (nG) {
@@ -440,6 +451,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
     };
     // contract k-steps [k0, k1) of the face table into the diagonal tiles and co
     auto face_contract = [&](int k0, int k1, double (&co)[NT][NT][2]) {
+      PDG_UNROLL(PDG_FACE_UNROLL)
       for (int kk = k0; kk < k1; ++kk) {
         const int qq = kk * 4 + t;
         const double al = sc1[qq], be = sc2[qq];

@@ -163,6 +163,12 @@ static std::string get_kernel(const std::string& policy, int dim, int P, bool sy
                                    "-DPDG_RHS_REGS_MAX=" + std::to_string(jit_rhs_regs_max()),
                                    "-I" + dir + "/csrc",
                                    "-I" + dir + "/../include"};
+  // PDG_JIT_DEFINES: extra space-separated -D options (tuning experiments)
+  if (const char* defs = getenv("PDG_JIT_DEFINES")) {
+    std::istringstream is(defs);
+    std::string tok;
+    while (is >> tok) opts.push_back(tok);
+  }
   std::string key = src;
   for (auto& o : opts) key += "\n" + o;
   {
