@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "assemble_kernel.cuh"
+#include "assemble_ws.cuh"
 
 namespace pdg {
 
@@ -127,20 +128,29 @@ static int jit_rhs_regs_max() {
   return v ? atoi(v) : PDG_RHS_REGS_MAX;
 }
 
+// PDG_WS=0 selects the single-warp body (assemble_body.cuh) instead of the
+// warp-specialised producer/consumer body (assemble_ws.cuh, default).
+static bool jit_ws() {
+  const char* v = getenv("PDG_WS");
+  return !(v && v[0] == '0');
+}
+
 static std::string full_source(const std::string& policy, int dim, int P, bool sym) {
-  // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow
-  // (register cap = 64K / (128 * n)); default 3 = 168 registers, 12 warps/SM
-  // (v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells)
+  // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow.
+  // single-warp body: CTA = 128 threads, default 3 (168 registers, 12 warps/SM;
+  //   v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells);
+  // warp-specialised body: CTA = 64 threads (one pair), default 8 (128 registers)
+  const bool ws = jit_ws();
   const char* mb = getenv("PDG_JIT_MINBLOCKS");
-  const int minblocks = mb ? std::max(1, atoi(mb)) : 3;
+  const int minblocks = mb ? std::max(1, atoi(mb)) : (ws ? 8 : 3);
   std::ostringstream os;
-  os << "#include \"assemble_body.cuh\"\n"
+  os << "#include \"" << (ws ? "assemble_ws.cuh" : "assemble_body.cuh") << "\"\n"
      << "namespace pdg_jit {\nusing namespace pdg;\n"
      << policy << "\n}\n"
-     << "extern \"C\" __global__ void __launch_bounds__(128, " << minblocks
+     << "extern \"C\" __global__ void __launch_bounds__(" << (ws ? 64 : 128) << ", " << minblocks
      << ") pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {\n"
-     << "  pdg::assemble_body<" << dim << ", " << P << ", " << (sym ? "true" : "false")
-     << ">(a, pdg_jit::JitCoef());\n}\n";
+     << "  pdg::" << (ws ? "assemble_ws<" : "assemble_body<") << dim << ", " << P << ", "
+     << (sym ? "true" : "false") << ">(a, pdg_jit::JitCoef());\n}\n";
   return os.str();
 }
 
@@ -275,17 +285,25 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
     KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values, write_col_idx,
                          rhs, err_flags, 0);
-    a.lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind,
-                        coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max());
-    const int threads = 128;
-    const size_t smem = (size_t)a.lay.warp_doubles * 8 * (threads / 32);
+    const bool ws = jit_ws();
+    const bool has_vr = coeffs->has_advection || coeffs->has_reaction;
+    a.lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, jit_rhs_regs_max());
+    int threads = 128;
+    size_t smem = (size_t)a.lay.warp_doubles * 8 * (threads / 32);
+    if (ws) {  // one producer/consumer pair per CTA: two stages + header + neighbour staging
+      int kv = 32;
+      a.lay.buf_doubles = ws_table_doubles(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, &kv);
+      a.lay.kv = kv;
+      threads = 64;
+      smem = (size_t)2 * (a.lay.buf_doubles + 64 + sizeof(WsHdr) / 8) * 8 + sizeof(NbrStage);
+    }
     Api& A = api();
     if (A.cuFuncSetAttribute(k.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES_, (int)smem) != 0)
       return fail(PDG_ERR_CUDA, "cuFuncSetAttribute(max dynamic smem) failed");
     int per_sm = 0;
     if (A.cuOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, threads, smem) != 0 || per_sm < 1) per_sm = 1;
-    const int64_t need = (pattern->n_row_elements + 3) / 4;
-    const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm * 8);
+    const int64_t need = ws ? pattern->n_row_elements : (pattern->n_row_elements + 3) / 4;
+    const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm * (ws ? 1 : 8));
     if (grid <= 0) return PDG_OK;
     void* args[] = {&a};
     if (A.cuLaunchKernel(k.fn, (unsigned)grid, 1, 1, threads, 1, 1, (unsigned)smem, (cudaStream_t)stream, args,

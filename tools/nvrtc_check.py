@@ -10,14 +10,17 @@ from paper_2007_04881_b200.model import policy_source  # noqa: E402
 from paper_2007_04881_b200.problems import WORKLOADS, coefficients  # noqa: E402
 
 
-def main(cfg="cfg5", degree=None, sym=True, minblocks=2):
+def main(cfg="cfg5", degree=None, sym=True, minblocks=2, ws="1"):
     w = WORKLOADS[cfg]
     p = w.degree if degree is None else int(degree)
     pol = policy_source(coefficients(w.coeffs, w.dim), w.dim)
-    src = ('#include "assemble_body.cuh"\nnamespace pdg_jit {\nusing namespace pdg;\n' + pol + '\n}\n'
-           f'extern "C" __global__ void __launch_bounds__(128, {minblocks}) pdg_jit_kernel('
+    body = "assemble_ws" if str(ws) == "1" else "assemble_body"
+    threads = 64 if str(ws) == "1" else 128
+    sym = str(sym) not in ("0", "False", "false")
+    src = (f'#include "{body}.cuh"\nnamespace pdg_jit {{\nusing namespace pdg;\n' + pol + '\n}\n'
+           f'extern "C" __global__ void __launch_bounds__({threads}, {minblocks}) pdg_jit_kernel('
            'const __grid_constant__ pdg::KArgs a) {\n'
-           f'  pdg::assemble_body<{w.dim}, {p}, {"true" if sym else "false"}>(a, pdg_jit::JitCoef());\n}}\n')
+           f'  pdg::{body}<{w.dim}, {p}, {"true" if sym else "false"}>(a, pdg_jit::JitCoef());\n}}\n')
     lib = C.CDLL("libnvrtc.so.12")
     prog = C.c_void_p()
     assert lib.nvrtcCreateProgram(C.byref(prog), src.encode(), b"pdg_jit.cu", 0, None, None) == 0
