@@ -128,11 +128,13 @@ static int jit_rhs_regs_max() {
   return v ? atoi(v) : PDG_RHS_REGS_MAX;
 }
 
-// PDG_WS=0 selects the single-warp body (assemble_body.cuh) instead of the
-// warp-specialised producer/consumer body (assemble_ws.cuh, default).
+// PDG_WS=1 selects the warp-specialised producer/consumer body
+// (assemble_ws.cuh) instead of the single-warp body (assemble_body.cuh).
+// Measured on 400k cfg5 cells (r1): single-warp 7.51 ms, WS 10.0 ms -- the
+// producer (tabulation + metadata) is the bottleneck, so WS is off by default.
 static bool jit_ws() {
   const char* v = getenv("PDG_WS");
-  return !(v && v[0] == '0');
+  return v && v[0] == '1';
 }
 
 static std::string full_source(const std::string& policy, int dim, int P, bool sym) {

@@ -117,25 +117,32 @@ __device__ __forceinline__ BoxConst<DIM> box_const(const double* box /*[2][DIM]*
   return b;
 }
 
-// 1D orthonormal Legendre values and derivatives on one box side
-// (three-term recurrence + companion derivative recurrence, basis.py:107-126).
+// 1D orthonormal Legendre values and derivatives on one box side.
+// polydg (basis.py:107-126,146-152) runs the three-term recurrence
+//   L_{k+1} = (2k+1)/(k+1) t L_k - k/(k+1) L_{k-1},  L'_{k+1} = (2k+1) L_k + L'_{k-1}
+// and scales afterwards by s_k = sqrt(2k+1)/sqrt(width) (and 1/half for L').
+// Here the recurrence runs directly on the scaled values v_k = s_k L_k,
+// dv_k = s_k L'_k / half: the ratios s_{k+1}/s_k are element independent
+// (the width cancels), so the scaling costs nothing per point.  Same values
+// up to rounding (<= a few ulp).  dv_0 = 0 is never formed (Tab::grad).
 template <int P>
 __device__ __forceinline__ void legendre_1d(double t, double rs, double ih, double* v, double* dv) {
-  double L[P + 1], dL[P + 1];
-  L[0] = 1.0; dL[0] = 0.0;
-  if (P >= 1) { L[1] = t; dL[1] = 1.0; }
-#pragma unroll
-  for (int k = 1; k < P; ++k) {
-    const double a = double(2 * k + 1) / double(k + 1);
-    const double b = double(k) / double(k + 1);
-    L[k + 1] = a * t * L[k] - b * L[k - 1];
-    dL[k + 1] = double(2 * k + 1) * L[k] + dL[k - 1];
+  v[0] = rs;
+  dv[0] = 0.0;
+  if (P >= 1) {
+    const double r1 = 1.7320508075688772 * rs;  // sqrt(3) / sqrt(width)
+    v[1] = r1 * t;
+    dv[1] = r1 * ih;
   }
 #pragma unroll
-  for (int k = 0; k <= P; ++k) {
-    const double s = sqrt(double(2 * k + 1)) * rs;  // compile-time sqrt, one mul
-    v[k] = L[k] * s;
-    dv[k] = dL[k] * (s * ih);
+  for (int k = 1; k < P; ++k) {
+    const double up = sqrt(double(2 * k + 3) / double(2 * k + 1));   // s_{k+1} / s_k
+    const double up2 = sqrt(double(2 * k + 3) / double(2 * k - 1));  // s_{k+1} / s_{k-1}
+    const double c1 = double(2 * k + 1) / double(k + 1) * up;
+    const double c2 = double(k) / double(k + 1) * up2;
+    v[k + 1] = (c1 * t) * v[k] - c2 * v[k - 1];
+    const double g = double(2 * k + 1) * up;
+    dv[k + 1] = k == 1 ? g * (ih * v[1]) : g * (ih * v[k]) + up2 * dv[k - 1];
   }
 }
 
@@ -157,6 +164,7 @@ struct Tab {
   }
   __device__ __forceinline__ double grad(int f, int k) const {
     constexpr MultiIdx<DIM, P> mi{};
+    if (mi.a[f][k] == 0) return 0.0;  // derivative of the constant mode (compile-time)
     double r = (k == 0 ? d1[0][mi.a[f][0]] : v1[0][mi.a[f][0]]) *
                (k == 1 ? d1[1][mi.a[f][1]] : v1[1][mi.a[f][1]]);
     if (DIM == 3) r *= (k == 2 ? d1[2][mi.a[f][2]] : v1[2][mi.a[f][2]]);

@@ -10,7 +10,7 @@ from paper_2007_04881_b200.model import policy_source  # noqa: E402
 from paper_2007_04881_b200.problems import WORKLOADS, coefficients  # noqa: E402
 
 
-def main(cfg="cfg5", degree=None, sym=True, minblocks=2, ws="1"):
+def main(cfg="cfg5", degree=None, sym=True, minblocks=3, ws="0"):
     w = WORKLOADS[cfg]
     p = w.degree if degree is None else int(degree)
     pol = policy_source(coefficients(w.coeffs, w.dim), w.dim)
