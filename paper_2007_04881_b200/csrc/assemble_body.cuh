@@ -60,6 +60,7 @@ namespace pdg {
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
 constexpr int NBR_WIN = 16;  // neighbour entries staged per window
+constexpr int FR_MAX = 32;   // simplex frames of one element kept in shared memory
 
 template <int DIM>
 struct Widths {
@@ -134,6 +135,14 @@ struct InterpCoef {
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+
+// 16-byte asynchronous global -> shared copies (LDGSTS), L2 only
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int DIM>
 __device__ __forceinline__ BoxConst<DIM> load_box(const double* erec, int64_t e) {
@@ -227,6 +236,9 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   double* sc2 = sc1 + 32;
   NbrStage* ns = reinterpret_cast<NbrStage*>(sc2 + 32);
   double* rhs_s = reinterpret_cast<double*>(ns + 1);  // [NB][32] when !RHS_REGS
+  // async-copied geometry: the element's simplex frames, the window's first facet frames
+  double* sfr = rhs_s + (S::RHS_REGS ? 0 : 32 * NB);
+  double* ffr = sfr + FR_MAX * W::SF;
 
   const int kv = a.lay.kv, kvp = a.lay.kv + 4;
   const int dk = cf.diff_kind();
@@ -238,8 +250,24 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   const int mode = a.mode;
 
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // cp.async the simplex frames of element kk into sfr (if they fit)
+  auto issue_frames = [&](int64_t kk) -> bool {
+    if (kk >= pat.n_row_elements) return false;
+    const int32_t en = pat.row_elements ? pat.row_elements[kk] : (int32_t)kk;
+    const int64_t s0n = m.elem_ptr[en];
+    const int nsn = (int)(m.elem_ptr[en + 1] - s0n);
+    if (nsn > FR_MAX) return false;
+    const double* src = a.sframe + s0n * W::SF;
+    for (int c = lane; c < nsn * W::SF / 2; c += 32) cp_async16(sfr + 2 * c, src + 2 * c);
+    cp_async_commit();
+    return true;
+  };
+  bool next_frames = issue_frames(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < pat.n_row_elements;
        k += nwarps) {
+    const bool fr_smem = next_frames;
+    cp_async_wait_all();
+    __syncwarp();
     const int32_t e = pat.row_elements ? pat.row_elements[k] : (int32_t)k;
     const int pe = B.degree[e];
     const int64_t dof_e = B.dof_offset[e];
@@ -275,7 +303,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           const int kq = gq - ls * nq;
           const double* xi = R.points + (int64_t)(r0 + kq) * 3;
           double x[3] = {0.0, 0.0, 0.0};
-          const double det = frame_point<DIM, DIM>(a.sframe + (s0 + ls) * W::SF, xi, x);
+          const double* fr = fr_smem ? sfr + ls * W::SF : a.sframe + (s0 + ls) * W::SF;
+          const double det = frame_point<DIM, DIM>(fr, xi, x);
           const double w = R.weights[r0 + kq] * det * valid;
           Tab<DIM, P> tb;
           tb.load(bx, x);
@@ -375,18 +404,10 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       }
     }
 
-    // warm L2 with the next element's simplex frames while the face phase runs
-    {
-      const int64_t kn = k + nwarps;
-      if (kn < pat.n_row_elements) {
-        const int32_t en = pat.row_elements ? pat.row_elements[kn] : (int32_t)kn;
-        const int64_t s0n = m.elem_ptr[en], s1n = m.elem_ptr[en + 1];
-        const char* p0 = reinterpret_cast<const char*>(a.sframe + s0n * W::SF);
-        const int64_t bytes = (s1n - s0n) * W::SF * 8;
-        for (int64_t off = (int64_t)lane * 128; off < bytes; off += 32 * 128) prefetch_l2(p0 + off);
-        if (lane == 0) prefetch_l2(a.erec + (int64_t)en * W::ER);
-      }
-    }
+    // the volume phase is done with sfr: start copying the next element's
+    // simplex frames while this element's faces are processed
+    __syncwarp();
+    next_frames = issue_frames(k + nwarps);
 
     // ------------------------------------------------------------ interfaces
     // Neighbour entries are staged NBR_WIN at a time (lane = entry): element,
@@ -404,11 +425,11 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
     const int slot = lane & (KF - 1);
 
     // tabulate one face slot: own trace (lanes 0-15) or neighbour trace (16-31)
-    auto tab_slot = [&](const double* nrm, int64_t frow, int r0, int kq, double valid, double sig, double sgn,
+    auto tab_slot = [&](const double* nrm, const double* frp, int r0, int kq, double valid, double sig, double sgn,
                         bool down, const BoxConst<DIM>& bo) {
       const double* xi = R.points + (int64_t)(r0 + kq) * 3;
       double x[3] = {0.0, 0.0, 0.0};
-      const double jac = frame_point<DIM, DIM - 1>(a.fframe + frow * W::FF, xi, x);
+      const double jac = frame_point<DIM, DIM - 1>(frp, xi, x);
       const double w = R.weights[r0 + kq] * jac * valid;
       Tab<DIM, P> tb;
       tb.load(mine ? bx : bo, x);
@@ -517,7 +538,13 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           ns->fb[lane] = fb;
           ns->info[lane] = info;
           ns->row0[lane] = row0;
+          if (!is_self) {  // first facet frame of the interface -> ffr[lane]
+            const double* src = a.fframe + (int64_t)row0 * W::FF;
+#pragma unroll
+            for (int c = 0; c < W::FF / 2; ++c) cp_async16(ffr + lane * W::FF + 2 * c, src + 2 * c);
+          }
         }
+        cp_async_commit();
         int incl = nj;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -530,6 +557,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         __syncwarp();
         if (selfm) colself = ns->col[__ffs(selfm) - 1];
       }
+      cp_async_wait_all();
       __syncwarp();
       // col_idx of this window's column span, all rows (division-free)
       if (a.write_cols) {
@@ -566,7 +594,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 #pragma unroll
           for (int i = 0; i < DIM; ++i) nrm[i] = ns->nrm[i][q];
           const BoxConst<DIM> bo = load_box<DIM>(a.erec, ns->j[q]);
-          tab_slot(nrm, ns->row0[q], r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, ns->sig[q],
+          tab_slot(nrm, ffr + q * W::FF, r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, ns->sig[q],
                    (info & 1) ? -1.0 : 1.0, (info & 2) != 0, bo);
           __syncwarp();
           face_contract(0, 2, co);
@@ -612,8 +640,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
             const int nvalid = min(KF, Pf - base);
             const int gq = base + min(slot, nvalid - 1);
             const int lr = gq / nq;
-            tab_slot(nrm, row0 + lr, r0, gq - lr * nq, slot < nvalid ? 1.0 : 0.0, sig, side ? -1.0 : 1.0,
-                     (info & 2) != 0, bo);
+            tab_slot(nrm, a.fframe + (row0 + lr) * W::FF, r0, gq - lr * nq, slot < nvalid ? 1.0 : 0.0, sig,
+                     side ? -1.0 : 1.0, (info & 2) != 0, bo);
             __syncwarp();
             face_contract(0, (nvalid + 3) >> 2, co);
             __syncwarp();

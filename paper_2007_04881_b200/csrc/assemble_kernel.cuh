@@ -28,7 +28,8 @@ inline AsmLayout make_layout(int dim, int P, int diff_kind, bool has_vr, int rhs
   int buf = vol > face ? vol : face;
   if (red > buf) buf = red;
   L.buf_doubles = buf;
-  L.warp_doubles = buf + 64 + (int)(sizeof(NbrStage) / 8) + (rhs_regs ? 0 : 32 * NB);
+  const int W = dim == 2 ? 8 : 16;  // frame record width (Widths<DIM>)
+  L.warp_doubles = buf + 64 + (int)(sizeof(NbrStage) / 8) + (rhs_regs ? 0 : 32 * NB) + FR_MAX * W + NBR_WIN * W;
   return L;
 }
 
