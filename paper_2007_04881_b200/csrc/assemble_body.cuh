@@ -219,7 +219,9 @@ __device__ __forceinline__ double face_flux(const CF& cf, const Tab<DIM, P>& tb,
   return fl;
 }
 
-template <int DIM, int P, bool SYM, class CF>
+// KV: volume slots per round when known at compile time (runtime-specialised
+// kernels), 0 = read a.lay.kv.
+template <int DIM, int P, bool SYM, class CF, int KV = 0>
 __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   using S = Shape<DIM, P>;
   using W = Widths<DIM>;
@@ -240,7 +242,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   double* sfr = rhs_s + (S::RHS_REGS ? 0 : 32 * NB);
   double* ffr = sfr + FR_MAX * W::SF;
 
-  const int kv = a.lay.kv, kvp = a.lay.kv + 4;
+  const int kv = KV ? KV : a.lay.kv, kvp = kv + 4;
   const int dk = cf.diff_kind();
   const int nG = dk != PDG_DIFF_NONE ? DIM : 0;
   const bool full = dk == PDG_DIFF_FULL;
@@ -364,8 +366,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         }
         __syncwarp();
         const int nk = (nvalid + 3) >> 2;
-        PDG_UNROLL(PDG_VOL_UNROLL)
-        for (int kk = 0; kk < nk; ++kk) {
+        auto vol_kstep = [&](int kk) {
           const int q = kk * 4 + t;
           if (nG) {
             const double s1 = sc1[q];
@@ -399,6 +400,15 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
               for (int cc = 0; cc < NT; ++cc)
                 if (!SYM || cc >= r) dmma(cd[r][cc], lf[r], rf[cc]);
           }
+        };
+        if (KV && nk == KV / 4) {
+          // full chunk of a runtime-specialised kernel: fixed trip count and
+          // compile-time table offsets
+#pragma unroll
+          for (int kk = 0; kk < KV / 4; ++kk) vol_kstep(kk);
+        } else {
+          PDG_UNROLL(PDG_VOL_UNROLL)
+          for (int kk = 0; kk < nk; ++kk) vol_kstep(kk);
         }
         __syncwarp();
       }

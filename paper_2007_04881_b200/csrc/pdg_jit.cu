@@ -137,7 +137,7 @@ static bool jit_ws() {
   return v && v[0] == '1';
 }
 
-static std::string full_source(const std::string& policy, int dim, int P, bool sym) {
+static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv) {
   // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow.
   // single-warp body: CTA = 128 threads, default 3 (168 registers, 12 warps/SM;
   //   v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells);
@@ -152,7 +152,9 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
      << "extern \"C\" __global__ void __launch_bounds__(" << (ws ? 64 : 128) << ", " << minblocks
      << ") pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {\n"
      << "  pdg::" << (ws ? "assemble_ws<" : "assemble_body<") << dim << ", " << P << ", "
-     << (sym ? "true" : "false") << ">(a, pdg_jit::JitCoef());\n}\n";
+     << (sym ? "true" : "false");
+  if (!ws) os << ", pdg_jit::JitCoef, " << kv;
+  os << ">(a, pdg_jit::JitCoef());\n}\n";
   return os.str();
 }
 
@@ -166,11 +168,11 @@ static bool read_file(const std::string& path, std::string& out) {
 }
 
 // compile or fetch; returns empty string on success, else the error
-static std::string get_kernel(const std::string& policy, int dim, int P, bool sym, JitKernel& out) {
+static std::string get_kernel(const std::string& policy, int dim, int P, bool sym, int kv, JitKernel& out) {
   Api& A = api();
   if (!A.ok) return "JIT unavailable: " + A.why;
   const std::string dir = lib_dir();
-  const std::string src = full_source(policy, dim, P, sym);
+  const std::string src = full_source(policy, dim, P, sym, kv);
   std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
                                    "-DPDG_RHS_REGS_MAX=" + std::to_string(jit_rhs_regs_max()),
                                    "-I" + dir + "/csrc",
@@ -263,7 +265,9 @@ extern "C" int pdg_jit_prepare(const pdg_coeffs* coeffs, const char* policy_sour
   PDG_TRY {
     if (!coeffs || !policy_source) return fail(PDG_ERR_INVALID, "null argument");
     JitKernel k;
-    const std::string err = get_kernel(policy_source, dim, max_degree, symmetric_accumulation(*coeffs), k);
+    const int kv = make_layout(dim, max_degree, coeffs->diffusion_kind,
+                               coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max()).kv;
+    const std::string err = get_kernel(policy_source, dim, max_degree, symmetric_accumulation(*coeffs), kv, k);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
     return PDG_OK;
   }
@@ -283,13 +287,13 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     if (write_col_idx && !pattern->col_idx) return fail(PDG_ERR_INVALID, "col_idx not allocated");
     JitKernel k;
     const bool sym = symmetric_accumulation(*coeffs);
-    const std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, sym, k);
-    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
-    KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values, write_col_idx,
-                         rhs, err_flags, 0);
     const bool ws = jit_ws();
     const bool has_vr = coeffs->has_advection || coeffs->has_reaction;
+    KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values, write_col_idx,
+                         rhs, err_flags, 0);
     a.lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, jit_rhs_regs_max());
+    const std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, sym, a.lay.kv, k);
+    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
     int threads = 128;
     size_t smem = (size_t)a.lay.warp_doubles * 8 * (threads / 32);
     if (ws) {  // one producer/consumer pair per CTA: two stages + header + neighbour staging

@@ -20,7 +20,7 @@ def main(cfg="cfg5", degree=None, sym=True, minblocks=3, ws="0"):
     src = (f'#include "{body}.cuh"\nnamespace pdg_jit {{\nusing namespace pdg;\n' + pol + '\n}\n'
            f'extern "C" __global__ void __launch_bounds__({threads}, {minblocks}) pdg_jit_kernel('
            'const __grid_constant__ pdg::KArgs a) {\n'
-           f'  pdg::{body}<{w.dim}, {p}, {"true" if sym else "false"}>(a, pdg_jit::JitCoef());\n}}\n')
+           f'  pdg::{body}<{w.dim}, {p}, {"true" if sym else "false"}{", pdg_jit::JitCoef, 32" if body == "assemble_body" else ""}>(a, pdg_jit::JitCoef());\n}}\n')
     lib = C.CDLL("libnvrtc.so.12")
     prog = C.c_void_p()
     assert lib.nvrtcCreateProgram(C.byref(prog), src.encode(), b"pdg_jit.cu", 0, None, None) == 0
