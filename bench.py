@@ -145,12 +145,16 @@ def hbm_peak():
         return 6650.0, "B200_PROFILING.md fallback"
 
 
-def ncu_traffic(config):
+def ncu_traffic(config, n_elements):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the element kernel from
+    the committed ncu --set full capture (profiles/ncu_element_kernel.json),
+    per launch of this workload: the capture's bytes per element x elements
+    (the capture runs a smaller mesh of the same generator and degree)."""
     p = os.path.join(ROOT, "profiles", "ncu_element_kernel.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d.get(config, {}).get("dram_bytes_per_launch")
+        return float(d[config]["dram_bytes_per_element"]) * n_elements
     except Exception:
         return None
 
@@ -362,7 +366,7 @@ def run_ours(args, w, rank, world, local_rank):
                    "mesh_build_s": round(mesh_s, 1)},
         "phases_ms": {"index": ms_index, "prepass": ms_pre, "element_kernel": ms_el},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(w.name),
+                     "frac": achieved / peak, "traffic": ncu_traffic(w.name, n_el),
                      "kernel": "assemble_elements (fused volume+face+boundary, DMMA f64)",
                      "algorithmic_flops_per_launch": work["flops"],
                      "algorithmic_bytes_per_launch": work["bytes"],
