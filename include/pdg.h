@@ -41,7 +41,7 @@ typedef unsigned long size_t;
 extern "C" {
 #endif
 
-#define PDG_ABI_VERSION 1
+#define PDG_ABI_VERSION 2
 
 typedef struct CUstream_st* pdg_stream; /* == cudaStream_t */
 
@@ -60,7 +60,9 @@ enum {
   PDG_FLAG_STRADDLE = 1u << 2,           /* ClassificationError model.py:128-135   */
   PDG_FLAG_UNCLASSIFIED = 1u << 3,       /* AssemblyError    assembly.py:680-684   */
   PDG_FLAG_NO_ADJACENT_SIMPLEX = 1u << 4,/* MeshError        model.py:224-225,253  */
-  PDG_FLAG_STACK = 1u << 5               /* coefficient program overflow (host bug) */
+  PDG_FLAG_STACK = 1u << 5,              /* coefficient program overflow (host bug) */
+  PDG_FLAG_NEG_DIFFUSION = 1u << 6       /* isotropic a(x) < 0 met by the sqrt-weighted volume
+                                            path: the host re-runs with PDG_OPT_PLAIN_VOLUME */
 };
 
 /* boundary tags (polydg mesh.py:40-45) */
@@ -140,6 +142,7 @@ typedef struct pdg_rules {
   const int32_t* vol_count;
   const int32_t* face_offset;  /* [max_order+1] interval (2D) / triangle (3D) rule */
   const int32_t* face_count;
+  const double* sqrt_weights;  /* [n] sqrt(weights) (sqrt-weighted symmetric volume tables) */
 } pdg_rules;
 
 typedef struct pdg_params {
@@ -147,7 +150,15 @@ typedef struct pdg_params {
   int32_t include_gradient_terms;
   double penalty_constant;     /* PenaltyConfig.constant (model.py:66) */
   const uint8_t* coverable;    /* [n_elements] or NULL (model.py:67) */
+  int32_t options;             /* PDG_OPT_* bits (kernel variants; 0 = default) */
+  int32_t pad_;
 } pdg_params;
+
+/* pdg_params.options */
+enum {
+  PDG_OPT_PLAIN_VOLUME = 1 /* isotropic volume term as (w a dphi) dphi^T instead of the
+                              symmetric sqrt(w a) dphi table (needed when a(x) < 0) */
+};
 
 /* Block pattern of the rows owned by one assembly (assembly.py:209-340). */
 typedef struct pdg_pattern {

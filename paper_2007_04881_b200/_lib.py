@@ -17,12 +17,15 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpdg.so")
 
 PDG_OK, PDG_ERR_INVALID, PDG_ERR_CUDA, PDG_ERR_UNSUPPORTED = 0, 1, 2, 3
+ABI_VERSION = 2  # include/pdg.h PDG_ABI_VERSION
 FLAG_DEGENERATE_SIMPLEX = 1 << 0
 FLAG_DEGENERATE_FACET = 1 << 1
 FLAG_STRADDLE = 1 << 2
 FLAG_UNCLASSIFIED = 1 << 3
 FLAG_NO_ADJACENT_SIMPLEX = 1 << 4
 FLAG_STACK = 1 << 5
+FLAG_NEG_DIFFUSION = 1 << 6
+OPT_PLAIN_VOLUME = 1
 
 MAX_CODE, MAX_CONST, MAX_STACK = 448, 96, 8
 DIFF_NONE, DIFF_ISO, DIFF_FULL = 0, 1, 2
@@ -67,12 +70,13 @@ class Coeffs(C.Structure):
 
 class Rules(C.Structure):
     _fields_ = [("max_order", _i32), ("points", _p), ("weights", _p),
-                ("vol_offset", _p), ("vol_count", _p), ("face_offset", _p), ("face_count", _p)]
+                ("vol_offset", _p), ("vol_count", _p), ("face_offset", _p), ("face_count", _p),
+                ("sqrt_weights", _p)]
 
 
 class Params(C.Structure):
     _fields_ = [("quad_increment", _i32), ("include_gradient_terms", _i32),
-                ("penalty_constant", _f64), ("coverable", _p)]
+                ("penalty_constant", _f64), ("coverable", _p), ("options", _i32), ("pad_", _i32)]
 
 
 class Pattern(C.Structure):
@@ -129,7 +133,7 @@ def load():
     for name in EXPORTS:
         if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes"):
             getattr(lib, name).restype = C.c_int
-    if lib.pdg_abi_version() != 1:
+    if lib.pdg_abi_version() != ABI_VERSION:
         raise EngineUnavailable("libpdg.so ABI version mismatch")
     return lib
 

@@ -321,12 +321,14 @@ class DeviceRules:
         self.t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(device)
                   for k, v in (("points", table.points if table.points.size else np.zeros((1, 3))),
                                ("weights", table.weights if table.weights.size else np.zeros(1)),
+                               ("sqrt_weights", np.sqrt(table.weights) if table.weights.size else np.zeros(1)),
                                ("vo", vo), ("vn", vn), ("fo", fo), ("fn", fn))}
         r = _lib.Rules()
         r.max_order = mo
         r.points, r.weights = _lib.ptr(self.t["points"]), _lib.ptr(self.t["weights"])
         r.vol_offset, r.vol_count = _lib.ptr(self.t["vo"]), _lib.ptr(self.t["vn"])
         r.face_offset, r.face_count = _lib.ptr(self.t["fo"]), _lib.ptr(self.t["fn"])
+        r.sqrt_weights = _lib.ptr(self.t["sqrt_weights"])
         self.struct = r
 
 
@@ -425,6 +427,8 @@ class SipgPlan:
         prm.quad_increment = inc
         prm.include_gradient_terms = 1
         prm.penalty_constant = float(pen.constant)
+        if os.environ.get("PDG_PLAIN_VOLUME") == "1":  # variant selection for experiments / tests
+            prm.options |= _lib.OPT_PLAIN_VOLUME
         if self.coverable is not None:
             self.t["coverable"] = T(self.coverable.astype(np.uint8))
             prm.coverable = _lib.ptr(self.t["coverable"])
@@ -539,7 +543,16 @@ class SipgPlan:
 
     def check_flags(self):
         self.stream.synchronize()
-        _raise_flags(int(self.t["flags"].item()))
+        flags = int(self.t["flags"].item())
+        if flags & _lib.FLAG_NEG_DIFFUSION and not self.params.options & _lib.OPT_PLAIN_VOLUME:
+            # the symmetric sqrt(w a) volume table needs a(x) >= 0: re-run the
+            # assembly with the plain (w a dphi) dphi^T variant (same kernel family)
+            self.params.options |= _lib.OPT_PLAIN_VOLUME
+            self.t["flags"].zero_()
+            self.run()
+            self.stream.synchronize()
+            flags = int(self.t["flags"].item())
+        _raise_flags(flags & ~_lib.FLAG_NEG_DIFFUSION)
 
     # -- results ----------------------------------------------------------------
     @property
@@ -776,12 +789,18 @@ def element_kernel(mesh, element, coeffs, spec, quad_increment=2):
     _lib.check(plan.lib.pdg_frames_build(C.byref(plan.dm.struct), C.byref(plan.basis),
                                          C.byref(plan.frames), _lib.ptr(plan.flags),
                                          _lib.stream_ptr(plan.stream)))
-    _lib.check(plan.lib.pdg_element_blocks(
-        C.byref(plan.dm.struct), C.byref(plan.basis), C.byref(plan.coeffs),
-        C.byref(plan.rules.struct), C.byref(plan.params), C.byref(plan.frames), _lib.ptr(ids), 1,
-        _lib.ptr(blocks), _lib.ptr(loads), _lib.ptr(plan.flags), _lib.stream_ptr(plan.stream)))
-    plan.stream.synchronize()
-    _raise_flags(int(plan.flags.item()))
+    for _ in range(2):
+        _lib.check(plan.lib.pdg_element_blocks(
+            C.byref(plan.dm.struct), C.byref(plan.basis), C.byref(plan.coeffs),
+            C.byref(plan.rules.struct), C.byref(plan.params), C.byref(plan.frames), _lib.ptr(ids), 1,
+            _lib.ptr(blocks), _lib.ptr(loads), _lib.ptr(plan.flags), _lib.stream_ptr(plan.stream)))
+        plan.stream.synchronize()
+        flags = int(plan.flags.item())
+        if not flags & _lib.FLAG_NEG_DIFFUSION or plan.params.options & _lib.OPT_PLAIN_VOLUME:
+            break
+        plan.params.options |= _lib.OPT_PLAIN_VOLUME  # a(x) < 0: plain volume variant
+        plan.flags.zero_()
+    _raise_flags(flags & ~_lib.FLAG_NEG_DIFFUSION)
     return blocks.cpu().numpy().reshape(nb, nb), loads.cpu().numpy()
 
 

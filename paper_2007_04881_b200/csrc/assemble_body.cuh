@@ -56,6 +56,11 @@ namespace pdg {
 #ifndef PDG_FACE_UNROLL
 #define PDG_FACE_UNROLL 1
 #endif
+// separate volume accumulators per gradient direction (breaks the DMMA
+// dependency chain c=0 -> c=1 inside a k-step; tuning knob)
+#ifndef PDG_VOL_SPLITC
+#define PDG_VOL_SPLITC 0
+#endif
 
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
@@ -249,6 +254,11 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   const bool has_vr = cf.has_adv() || cf.has_reac();
   const int rAG = nG, rV = nG + (full ? DIM : 0), rR = rV + 1;
   const bool grad_terms = dk != PDG_DIFF_NONE && a.prm.include_gradient_terms;
+  // Isotropic diffusion: the volume table holds sqrt(w a) dphi, so the
+  // k-step feeds the same fragment as both DMMA operands (no per-k-step
+  // weighting, half the fragment loads).  Needs a(x) >= 0; a negative value
+  // raises PDG_FLAG_NEG_DIFFUSION and the host re-runs with PDG_OPT_PLAIN_VOLUME.
+  const bool sqrtw = dk == PDG_DIFF_ISO && !(a.prm.options & PDG_OPT_PLAIN_VOLUME);
   const int mode = a.mode;
 
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -280,6 +290,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 
     double cd[NT][NT][2];
     zero_tiles<NT>(cd);
+    double cd2[NT][NT][2];  // used only with PDG_VOL_SPLITC
+    zero_tiles<NT>(cd2);
     double racc[S::RHS_REGS ? NB : 1];
 #pragma unroll
     for (int f = 0; f < (S::RHS_REGS ? NB : 1); ++f) racc[f] = 0.0;
@@ -311,7 +323,17 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           Tab<DIM, P> tb;
           tb.load(bx, x);
           double* col = buf + lane;
-          if (nG) {
+          if (nG && sqrtw) {
+            const double av = cf.a_iso(x);
+            if (av < 0.0) raise_flag(a.flags, PDG_FLAG_NEG_DIFFUSION);
+            const double sw = R.sqrt_weights[r0 + kq] * fr[DIM + DIM * DIM + 1] * sqrt(fmax(av, 0.0)) * valid;
+            Tab<DIM, P> ts = tb;
+            ts.scale(sw);
+#pragma unroll
+            for (int c = 0; c < DIM; ++c)
+#pragma unroll
+              for (int f = 0; f < NBP; ++f) col[(c * NBP + f) * kvp] = f < NB ? ts.grad(f, c) : 0.0;
+          } else if (nG) {
             const double av = dk == PDG_DIFF_ISO ? cf.a_iso(x) : 1.0;
             sc1[lane] = w * av;
 #pragma unroll
@@ -368,7 +390,22 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         const int nk = (nvalid + 3) >> 2;
         auto vol_kstep = [&](int kk) {
           const int q = kk * 4 + t;
-          if (nG) {
+          if (nG && sqrtw) {
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+              double fr_[NT];
+#pragma unroll
+              for (int i = 0; i < NT; ++i) fr_[i] = buf[(c * NBP + i * 8 + g) * kvp + q];
+#pragma unroll
+              for (int r = 0; r < NT; ++r)
+#pragma unroll
+                for (int cc = 0; cc < NT; ++cc)
+                  if (!SYM || cc >= r) {
+                    if (PDG_VOL_SPLITC && (c & 1)) dmma(cd2[r][cc], fr_[r], fr_[cc]);
+                    else dmma(cd[r][cc], fr_[r], fr_[cc]);
+                  }
+            }
+          } else if (nG) {
             const double s1 = sc1[q];
 #pragma unroll
             for (int c = 0; c < DIM; ++c) {
@@ -414,6 +451,15 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       }
     }
 
+    if constexpr (PDG_VOL_SPLITC) {
+#pragma unroll
+      for (int r = 0; r < NT; ++r)
+#pragma unroll
+        for (int cc = 0; cc < NT; ++cc) {
+          cd[r][cc][0] += cd2[r][cc][0];
+          cd[r][cc][1] += cd2[r][cc][1];
+        }
+    }
     // the volume phase is done with sfr: start copying the next element's
     // simplex frames while this element's faces are processed
     __syncwarp();

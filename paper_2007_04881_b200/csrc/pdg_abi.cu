@@ -151,7 +151,7 @@ extern "C" int pdg_assemble(const pdg_mesh* mesh, const pdg_basis* basis, const 
   PDG_TRY {
     int rc = check_common(mesh, basis, coeffs);
     if (rc) return rc;
-    if (!rules || !params || !pattern || !frames || !sigma || !face_flow || !values || !rhs)
+    if (!rules || !rules->sqrt_weights || !params || !pattern || !frames || !sigma || !face_flow || !values || !rhs)
       return fail(PDG_ERR_INVALID, "null argument");
     if (write_col_idx && !pattern->col_idx) return fail(PDG_ERR_INVALID, "col_idx not allocated");
     const KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values,
@@ -172,7 +172,7 @@ extern "C" int pdg_element_blocks(const pdg_mesh* mesh, const pdg_basis* basis, 
   PDG_TRY {
     int rc = check_common(mesh, basis, coeffs);
     if (rc) return rc;
-    if (!rules || !params || !frames || !elements || !blocks || !loads)
+    if (!rules || !rules->sqrt_weights || !params || !frames || !elements || !blocks || !loads)
       return fail(PDG_ERR_INVALID, "null argument");
     pdg_pattern pat;
     std::memset(&pat, 0, sizeof(pat));

@@ -282,7 +282,7 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
   PDG_TRY {
     int rc = check_common(mesh, basis, coeffs);
     if (rc) return rc;
-    if (!policy_source || !rules || !params || !pattern || !frames || !sigma || !face_flow || !values || !rhs)
+    if (!policy_source || !rules || !rules->sqrt_weights || !params || !pattern || !frames || !sigma || !face_flow || !values || !rhs)
       return fail(PDG_ERR_INVALID, "null argument");
     if (write_col_idx && !pattern->col_idx) return fail(PDG_ERR_INVALID, "col_idx not allocated");
     JitKernel k;

@@ -266,6 +266,7 @@ __global__ void frames_kernel(const pdg_mesh m, const pdg_basis B, const pdg_fra
 #pragma unroll
       for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
     o[DIM + DIM * DIM] = det;
+    o[DIM + DIM * DIM + 1] = sqrt(det);  // sqrt-weighted volume tables (assemble_body.cuh)
   }
   for (int64_t r = tid; r < m.n_facets; r += stride) {
     double v0[3], E[3][3];

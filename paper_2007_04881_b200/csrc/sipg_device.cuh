@@ -156,6 +156,14 @@ struct Tab {
 #pragma unroll
     for (int i = 0; i < DIM; ++i) legendre_1d<P>((x[i] - b.c[i]) * b.ih[i], b.rs[i], b.ih[i], v1[i], d1[i]);
   }
+  // multiply every basis function (and gradient) by s: scale the dim-0 factors
+  __device__ __forceinline__ void scale(double s) {
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+      v1[0][k] *= s;
+      d1[0][k] *= s;
+    }
+  }
   __device__ __forceinline__ double val(int f) const {
     constexpr MultiIdx<DIM, P> mi{};
     double r = v1[0][mi.a[f][0]] * v1[1][mi.a[f][1]];
@@ -248,10 +256,20 @@ __device__ __forceinline__ double facet_frame(const pdg_mesh& m, int64_t row, do
 // With A[i][k] = L_i(item k) and B[k][j] = R_j(item k), a thread that owns
 // (function f0+g, item k0+t) feeds both operands from the same table slot.
 // ---------------------------------------------------------------------------
+// PDG_DMMA_VOLATILE=0 lets the compiler reorder independent DMMAs (tuning knob)
+#ifndef PDG_DMMA_VOLATILE
+#define PDG_DMMA_VOLATILE 1
+#endif
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+#if PDG_DMMA_VOLATILE
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
+#else
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+#endif
 }
 
 }  // namespace pdg

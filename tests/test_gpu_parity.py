@@ -102,6 +102,33 @@ def test_hyperbolic_inflow_outflow(name, p):
     _run(pm, F.hyperbolic(pm.dim), p)
 
 
+def test_sign_changing_diffusion_reruns_plain_volume():
+    """a(x) < 0 somewhere: the sqrt(w a) volume table cannot hold it, the
+    device flags it and the plan re-runs the plain variant (same result)."""
+    import paper_2007_04881_b200.model as M
+
+    coeffs = M.PdeCoefficients(diffusion=M.scalar_diffusion(F.X - 0.3, 2), source=M.constant_scalar(1.0),
+                               dirichlet_data=M.constant_scalar(0.0))
+    _run(_mesh("clusters10"), coeffs, 3)
+
+
+@pytest.mark.parametrize("env", [{"PDG_JIT": "0"}, {"PDG_PLAIN_VOLUME": "1"},
+                                 {"PDG_JIT": "0", "PDG_PLAIN_VOLUME": "1"}])
+@pytest.mark.parametrize("case", ["vardiff", "adr", "aniso3d"])
+def test_kernel_variants(monkeypatch, env, case):
+    """The ahead-of-time (bytecode-interpreted) kernels and the plain volume
+    variant match the oracle like the default NVRTC-specialised kernel."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    if case == "vardiff":
+        _run(_mesh("clusters10"), F.variable_diffusion(2), 3)
+    elif case == "adr":
+        _run(_mesh("clusters10"), F.adr(2), 2)
+    else:
+        pm = _mesh("cube3")
+        _run(pm, F.anisotropic(3), 1, predicate=lambda x: x[0] < 0.5)
+
+
 def test_variable_degree():
     """Per-element degrees (reference test_assembly.py:440-450)."""
     pm = agglomerate(F.square_grid(4), F.square_blocks(4, 2))

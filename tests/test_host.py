@@ -35,7 +35,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     lib = _lib.load()
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.pdg_abi_version() == 1
+    assert lib.pdg_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_library_rejects_bad_arguments_without_a_gpu():

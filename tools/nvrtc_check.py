@@ -27,6 +27,7 @@ def main(cfg="cfg5", degree=None, sym=True, minblocks=3, ws="0"):
     d = os.path.join(ROOT, "paper_2007_04881_b200")
     opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", f"-DPDG_RHS_REGS_MAX={os.environ.get('PDG_RHS_REGS_MAX', 20)}".encode(),
             f"-I{d}/csrc".encode(), f"-I{d}/../include".encode(), b"-Xptxas=-v"]
+    opts += [t.encode() for t in os.environ.get("PDG_JIT_DEFINES", "").split()]
     arr = (C.c_char_p * len(opts))(*opts)
     rc = lib.nvrtcCompileProgram(prog, len(opts), arr)
     n = C.c_size_t()
@@ -34,6 +35,13 @@ def main(cfg="cfg5", degree=None, sym=True, minblocks=3, ws="0"):
     log = C.create_string_buffer(n.value)
     lib.nvrtcGetProgramLog(prog, log)
     print("rc", rc)
+    if rc == 0:
+        sz = C.c_size_t()
+        lib.nvrtcGetCUBINSize(prog, C.byref(sz))
+        buf = C.create_string_buffer(sz.value)
+        lib.nvrtcGetCUBIN(prog, buf)
+        with open(os.environ.get("PDG_CUBIN_OUT", "/tmp/pdg_jit.cubin"), "wb") as fh:
+            fh.write(buf.raw)
     print(log.value.decode()[-3000:])
     return rc
 
