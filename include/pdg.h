@@ -160,6 +160,25 @@ enum {
                               symmetric sqrt(w a) dphi table (needed when a(x) < 0) */
 };
 
+/* Per adjacency entry (row element e, sorted neighbour j) of the rows of one
+ * assembly: the block position and the metadata of the interface's first face,
+ * flattened by pdg_iface_records so the element kernel stages a window of
+ * neighbours with one contiguous asynchronous copy instead of chains of
+ * dependent gathers (nbr -> interface -> face -> sigma / normal / frame).
+ * 64 bytes.  Self entry: j == e, fa == fb. */
+typedef struct pdg_iface_rec {
+  int32_t j;        /* neighbour element (sorted ascending, self included) */
+  int32_t nj;       /* its number of basis functions */
+  int32_t col;      /* first column of its block within e's rows (assembly.py:316-321) */
+  int32_t pj;       /* its degree */
+  int32_t fa, fb;   /* face range [fa, fb) of the interface (mesh iface_ptr) */
+  int32_t row0;     /* first sub-facet row of face fa */
+  int32_t info;     /* bit0: e is face fa's neighbour side; bit1: e is downwind of fa;
+                       bit2: single face, single sub-facet, <= 8 face points (paired rounds) */
+  double sig;       /* penalty of face fa (model.py:238-257) */
+  double nrm[3];    /* owner normal of face fa */
+} pdg_iface_rec;
+
 /* Block pattern of the rows owned by one assembly (assembly.py:209-340). */
 typedef struct pdg_pattern {
   int64_t n_row_elements;
@@ -172,6 +191,7 @@ typedef struct pdg_pattern {
   int64_t* elem_row_offset;    /* [n_row_elements+1] first local row of the element */
   int64_t* row_ptr;            /* [n_local_rows+1] */
   int64_t* col_idx;            /* [nnz] */
+  pdg_iface_rec* nbr_rec;      /* [nbr_ptr[n_elements]] from pdg_iface_records (entries of owned rows) */
 } pdg_pattern;
 
 /* Affine frames, produced once per assembly by pdg_frames_build and read by
@@ -227,6 +247,12 @@ int pdg_face_prepass(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coe
                      const pdg_rules* rules, const pdg_params* params, double* sigma,
                      int8_t* face_flow, double* elem_abar, uint32_t* err_flags,
                      pdg_stream stream);
+
+/* Interface records of the owned rows (pdg_iface_rec), after pdg_adjacency and
+ * pdg_face_prepass (sigma, flow side).  Fills pattern->nbr_rec. */
+int pdg_iface_records(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                      const pdg_rules* rules, const pdg_params* params, const pdg_pattern* pattern,
+                      const double* sigma, const int8_t* face_flow, pdg_stream stream);
 
 /* Geometry pre-pass: fills pdg_frames; degenerate simplices / facets raise
  * PDG_FLAG_DEGENERATE_* (quadrature.py:133-134,152-153). */

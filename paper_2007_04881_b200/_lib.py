@@ -83,7 +83,7 @@ class Pattern(C.Structure):
     _fields_ = [("n_row_elements", _i64), ("row_elements", _p),
                 ("nbr_ptr", _p), ("nbr_elem", _p), ("nbr_iface", _p),
                 ("row_len", _p), ("elem_val_offset", _p), ("elem_row_offset", _p),
-                ("row_ptr", _p), ("col_idx", _p)]
+                ("row_ptr", _p), ("col_idx", _p), ("nbr_rec", _p)]
 
 
 class Frames(C.Structure):
@@ -92,7 +92,7 @@ class Frames(C.Structure):
 
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
 EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes", "pdg_adjacency",
-           "pdg_pattern_offsets", "pdg_pattern_fill", "pdg_face_prepass", "pdg_frames_build",
+           "pdg_pattern_offsets", "pdg_pattern_fill", "pdg_face_prepass", "pdg_iface_records", "pdg_frames_build",
            "pdg_assemble", "pdg_assemble_jit", "pdg_jit_prepare",
            "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks")
 
@@ -120,6 +120,8 @@ def load():
     lib.pdg_pattern_fill.argtypes = [P(Mesh), P(Basis), P(Pattern), _p]
     lib.pdg_face_prepass.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params),
                                      _p, _p, _p, _p, _p]
+    lib.pdg_iface_records.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params), P(Pattern),
+                                      _p, _p, _p]
     lib.pdg_frames_build.argtypes = [P(Mesh), P(Basis), P(Frames), _p, _p]
     lib.pdg_assemble.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params), P(Pattern),
                                  P(Frames), _p, _p, _p, _i32, _p, _p, _p]

@@ -451,6 +451,7 @@ class SipgPlan:
         self.t.update(nbr_ptr=z(nel + 1, i64), nbr_elem=z(nadj, i32), nbr_iface=z(nadj, i32),
                       row_len=z(nr, i64), val_off=z(nr + 1, i64), row_off=z(nr + 1, i64),
                       row_ptr=z(self.n_local_rows + 1, i64),
+                      nbr_rec=z(nadj * 8, torch.float64),  # pdg_iface_rec, 64 B per entry
                       sigma=z(flat.n_faces, torch.float64), flow=z(flat.n_faces, torch.int8),
                       abar=z(nel, torch.float64), flags=torch.zeros(1, dtype=torch.int32, device=dev))
         W = 8 if d == 2 else 16
@@ -472,6 +473,7 @@ class SipgPlan:
         pat.row_len, pat.elem_val_offset, pat.elem_row_offset = (
             _lib.ptr(self.t["row_len"]), _lib.ptr(self.t["val_off"]), _lib.ptr(self.t["row_off"]))
         pat.row_ptr = _lib.ptr(self.t["row_ptr"])
+        pat.nbr_rec = _lib.ptr(self.t["nbr_rec"])
         self.pattern = pat
 
         # size query (the one sync, like polydg's pattern build before values)
@@ -510,6 +512,10 @@ class SipgPlan:
             C.byref(self.rules.struct), C.byref(self.params), _lib.ptr(self.t["sigma"]),
             _lib.ptr(self.t["flow"]), _lib.ptr(self.t["abar"]), _lib.ptr(self.t["flags"]),
             _lib.stream_ptr(self.stream)))
+        _lib.check(self.lib.pdg_iface_records(
+            C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs),
+            C.byref(self.rules.struct), C.byref(self.params), C.byref(self.pattern),
+            _lib.ptr(self.t["sigma"]), _lib.ptr(self.t["flow"]), _lib.stream_ptr(self.stream)))
 
     def _elements(self, write_col_idx=True):
         import ctypes as C

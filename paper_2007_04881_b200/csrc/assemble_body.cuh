@@ -56,11 +56,6 @@ namespace pdg {
 #ifndef PDG_FACE_UNROLL
 #define PDG_FACE_UNROLL 1
 #endif
-// separate volume accumulators per gradient direction (breaks the DMMA
-// dependency chain c=0 -> c=1 inside a k-step; tuning knob)
-#ifndef PDG_VOL_SPLITC
-#define PDG_VOL_SPLITC 0
-#endif
 
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
@@ -241,8 +236,9 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   double* buf = smem + (threadIdx.x >> 5) * a.lay.warp_doubles;
   double* sc1 = buf + a.lay.buf_doubles;
   double* sc2 = sc1 + 32;
-  NbrStage* ns = reinterpret_cast<NbrStage*>(sc2 + 32);
-  double* rhs_s = reinterpret_cast<double*>(ns + 1);  // [NB][32] when !RHS_REGS
+  // interface records of the current / next element's first neighbour window
+  pdg_iface_rec* recs = reinterpret_cast<pdg_iface_rec*>(sc2 + 32);  // [2][NBR_WIN]
+  double* rhs_s = reinterpret_cast<double*>(recs + 2 * NBR_WIN);    // [NB][32] when !RHS_REGS
   // async-copied geometry: the element's simplex frames, the window's first facet frames
   double* sfr = rhs_s + (S::RHS_REGS ? 0 : 32 * NB);
   double* ffr = sfr + FR_MAX * W::SF;
@@ -262,25 +258,50 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   const int mode = a.mode;
 
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // cp.async the simplex frames of element kk into sfr (if they fit)
-  auto issue_frames = [&](int64_t kk) -> bool {
+  // Asynchronous staging one element ahead (cp.async, issued while the
+  // current element's faces run): the simplex frames of element kk into sfr
+  // (if they fit) and the interface records of its first neighbour window
+  // into recs[rb].  The caller commits the group.
+  auto issue_next = [&](int64_t kk, int rb) -> bool {
     if (kk >= pat.n_row_elements) return false;
     const int32_t en = pat.row_elements ? pat.row_elements[kk] : (int32_t)kk;
+    if (!mode) {
+      const int64_t r0n = pat.nbr_ptr[en];
+      const int nwn = min(NBR_WIN, (int)(pat.nbr_ptr[en + 1] - r0n));
+      const double* rsrc = reinterpret_cast<const double*>(pat.nbr_rec + r0n);
+      double* rdst = reinterpret_cast<double*>(recs + rb * NBR_WIN);
+      for (int c = lane; c < nwn * 4; c += 32) cp_async16(rdst + 2 * c, rsrc + 2 * c);
+    }
     const int64_t s0n = m.elem_ptr[en];
     const int nsn = (int)(m.elem_ptr[en + 1] - s0n);
     if (nsn > FR_MAX) return false;
     const double* src = a.sframe + s0n * W::SF;
     for (int c = lane; c < nsn * W::SF / 2; c += 32) cp_async16(sfr + 2 * c, src + 2 * c);
-    cp_async_commit();
     return true;
   };
-  bool next_frames = issue_frames(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  // first facet frame of every non-self interface of a staged window -> ffr[entry]
+  auto issue_ffr = [&](const pdg_iface_rec* rw, int nw, int32_t e) {
+    if (lane < nw && rw[lane].j != e) {
+      const double* src = a.fframe + (int64_t)rw[lane].row0 * W::FF;
+#pragma unroll
+      for (int c = 0; c < W::FF / 2; ++c) cp_async16(ffr + lane * W::FF + 2 * c, src + 2 * c);
+    }
+  };
+  int rb = 0;
+  bool next_frames = issue_next(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, rb);
+  cp_async_commit();
   for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < pat.n_row_elements;
-       k += nwarps) {
+       k += nwarps, rb ^= 1) {
     const bool fr_smem = next_frames;
     cp_async_wait_all();
     __syncwarp();
     const int32_t e = pat.row_elements ? pat.row_elements[k] : (int32_t)k;
+    pdg_iface_rec* rc = recs + rb * NBR_WIN;
+    const int64_t q0 = mode ? 0 : pat.nbr_ptr[e];
+    const int nnb = mode ? 0 : (int)(pat.nbr_ptr[e + 1] - q0);
+    // the first window's facet frames land during the volume phase
+    issue_ffr(rc, min(NBR_WIN, nnb), e);
+    cp_async_commit();
     const int pe = B.degree[e];
     const int64_t dof_e = B.dof_offset[e];
     const int ne = (int)(B.dof_offset[e + 1] - dof_e);
@@ -290,8 +311,6 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 
     double cd[NT][NT][2];
     zero_tiles<NT>(cd);
-    double cd2[NT][NT][2];  // used only with PDG_VOL_SPLITC
-    zero_tiles<NT>(cd2);
     double racc[S::RHS_REGS ? NB : 1];
 #pragma unroll
     for (int f = 0; f < (S::RHS_REGS ? NB : 1); ++f) racc[f] = 0.0;
@@ -400,10 +419,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
               for (int r = 0; r < NT; ++r)
 #pragma unroll
                 for (int cc = 0; cc < NT; ++cc)
-                  if (!SYM || cc >= r) {
-                    if (PDG_VOL_SPLITC && (c & 1)) dmma(cd2[r][cc], fr_[r], fr_[cc]);
-                    else dmma(cd[r][cc], fr_[r], fr_[cc]);
-                  }
+                  if (!SYM || cc >= r) dmma(cd[r][cc], fr_[r], fr_[cc]);
             }
           } else if (nG) {
             const double s1 = sc1[q];
@@ -451,32 +467,22 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       }
     }
 
-    if constexpr (PDG_VOL_SPLITC) {
-#pragma unroll
-      for (int r = 0; r < NT; ++r)
-#pragma unroll
-        for (int cc = 0; cc < NT; ++cc) {
-          cd[r][cc][0] += cd2[r][cc][0];
-          cd[r][cc][1] += cd2[r][cc][1];
-        }
-    }
     // the volume phase is done with sfr: start copying the next element's
-    // simplex frames while this element's faces are processed
+    // simplex frames and records while this element's faces are processed
     __syncwarp();
-    next_frames = issue_frames(k + nwarps);
+    next_frames = issue_next(k + nwarps, rb ^ 1);
+    cp_async_commit();
 
     // ------------------------------------------------------------ interfaces
-    // Neighbour entries are staged NBR_WIN at a time (lane = entry): element,
-    // DoF count, column start, face range and the first face's metadata, so
-    // the face loop below reads shared memory instead of chains of dependent
-    // global loads.  Two interfaces made of a single sub-facet with <= 8
+    // Neighbour entries are staged NBR_WIN at a time as interface records
+    // (pdg_iface_rec: element, DoF count, column start, face range and the
+    // first face's metadata, flattened by pdg_iface_records; the first window
+    // arrives by cp.async during the previous element's faces), so the face
+    // loop reads shared memory instead of chains of dependent global loads.  Two interfaces made of a single sub-facet with <= 8
     // quadrature points (every 2D Voronoi interface up to p = 6) share one
     // tabulation round: slots 0-7 / 8-15, own trace on lanes 0-15, the
     // neighbour's on lanes 16-31.
     int64_t colself = 0;
-    const int64_t q0 = mode ? 0 : pat.nbr_ptr[e];
-    const int nnb = mode ? 0 : (int)(pat.nbr_ptr[e + 1] - q0);
-    int colcarry = 0;
     const bool mine = lane < KF;
     const int slot = lane & (KF - 1);
 
@@ -563,125 +569,93 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 
     for (int w0 = 0; w0 < nnb; w0 += NBR_WIN) {
       const int nw = min(NBR_WIN, nnb - w0);
-      {
-        int nj = 0;
-        bool is_self = false;
-        if (lane < nw) {
-          const int32_t j = pat.nbr_elem[q0 + w0 + lane];
-          const int32_t ifc = pat.nbr_iface[q0 + w0 + lane];
-          nj = (int)(B.dof_offset[j + 1] - B.dof_offset[j]);
-          is_self = j == e;
-          ns->j[lane] = j;
-          ns->nj[lane] = nj;
-          const int pj = B.degree[j];
-          ns->pj[lane] = pj;
-          int fa = 0, fb = 0, info = 0, row0 = 0, nrows = 0;
-          if (!is_self) {
-            fa = (int)m.iface_ptr[ifc];
-            fb = (int)m.iface_ptr[ifc + 1];
-            const int side = m.face_owner[fa] == e ? 0 : 1;
-            const bool down = cf.has_adv() && a.flow[fa] == side;
-            row0 = (int)m.face_ptr[fa];
-            nrows = (int)(m.face_ptr[fa + 1] - row0);
-            const int nq = R.face_count[2 * max(pe, pj) + a.prm.quad_increment];
-            const bool simple = fb - fa == 1 && nrows == 1 && nq <= 8;
-            info = side | (down ? 2 : 0) | (simple ? 4 : 0);
-            ns->sig[lane] = a.sigma[fa];
-#pragma unroll
-            for (int i = 0; i < DIM; ++i) ns->nrm[i][lane] = m.face_normal[(int64_t)fa * DIM + i];
-          }
-          ns->fa[lane] = fa;
-          ns->fb[lane] = fb;
-          ns->info[lane] = info;
-          ns->row0[lane] = row0;
-          if (!is_self) {  // first facet frame of the interface -> ffr[lane]
-            const double* src = a.fframe + (int64_t)row0 * W::FF;
-#pragma unroll
-            for (int c = 0; c < W::FF / 2; ++c) cp_async16(ffr + lane * W::FF + 2 * c, src + 2 * c);
-          }
-        }
-        cp_async_commit();
-        int incl = nj;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        if (lane < nw) ns->col[lane] = colcarry + incl - nj;
-        colcarry += __shfl_sync(0xffffffffu, incl, 31);
-        const unsigned selfm = __ballot_sync(0xffffffffu, is_self);
+      if (w0 == 0) {
+        // this element's facet frames; the next element's copies stay in flight
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        // windows beyond the first (more than NBR_WIN neighbours): synchronous restage
         __syncwarp();
-        if (selfm) colself = ns->col[__ffs(selfm) - 1];
+        const double* rsrc = reinterpret_cast<const double*>(pat.nbr_rec + q0 + w0);
+        for (int c = lane; c < nw * 4; c += 32) cp_async16(reinterpret_cast<double*>(rc) + 2 * c, rsrc + 2 * c);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        issue_ffr(rc, nw, e);
+        cp_async_commit();
+        cp_async_wait_all();
       }
-      cp_async_wait_all();
       __syncwarp();
+      {
+        const unsigned selfm = __ballot_sync(0xffffffffu, lane < nw && rc[lane].j == e);
+        if (selfm) colself = rc[__ffs(selfm) - 1].col;
+      }
       // col_idx of this window's column span, all rows (division-free)
       if (a.write_cols) {
-        const int c0 = ns->col[0];
-        const int c1 = ns->col[nw - 1] + ns->nj[nw - 1];
+        const int c0 = rc[0].col;
+        const int c1 = rc[nw - 1].col + rc[nw - 1].nj;
         int q = 0;
         for (int p = c0 + lane; p < c1; p += 32) {
-          while (q + 1 < nw && ns->col[q + 1] <= p) ++q;
-          const int64_t cv = B.dof_offset[ns->j[q]] + (p - ns->col[q]);
+          while (q + 1 < nw && rc[q + 1].col <= p) ++q;
+          const int64_t cv = B.dof_offset[rc[q].j] + (p - rc[q].col);
           int64_t* dst = pat.col_idx + voff + p;
           for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
         }
       }
       int qi = 0;
       while (qi < nw) {
-        if (ns->j[qi] == e) {
+        if (rc[qi].j == e) {
           ++qi;
           continue;
         }
         int qb = qi + 1;
-        if (qb < nw && ns->j[qb] == e) ++qb;
-        const bool pair = (ns->info[qi] & 4) && qb < nw && (ns->info[qb] & 4);
+        if (qb < nw && rc[qb].j == e) ++qb;
+        const bool pair = (rc[qi].info & 4) && qb < nw && (rc[qb].info & 4);
         double co[NT][NT][2];
         zero_tiles<NT>(co);
         if (pair) {
           // ---- two single-facet interfaces in one round
           const int seg = slot >> 3, ls = slot & 7;
           const int q = seg ? qb : qi;
-          const int info = ns->info[q];
-          const int pj = ns->pj[q];
+          const int info = rc[q].info;
+          const int pj = rc[q].pj;
           const int order = 2 * max(pe, pj) + a.prm.quad_increment;
           const int r0 = R.face_offset[order], nq = R.face_count[order];
           double nrm[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-          for (int i = 0; i < DIM; ++i) nrm[i] = ns->nrm[i][q];
-          const BoxConst<DIM> bo = load_box<DIM>(a.erec, ns->j[q]);
-          tab_slot(nrm, ffr + q * W::FF, r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, ns->sig[q],
+          for (int i = 0; i < DIM; ++i) nrm[i] = rc[q].nrm[i];
+          const BoxConst<DIM> bo = load_box<DIM>(a.erec, rc[q].j);
+          tab_slot(nrm, ffr + q * W::FF, r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, rc[q].sig,
                    (info & 1) ? -1.0 : 1.0, (info & 2) != 0, bo);
           __syncwarp();
           face_contract(0, 2, co);
-          store_block<NT, false>(a.values, voff, Lrow, ns->col[qi], ne, ns->nj[qi], co, g, t);
+          store_block<NT, false>(a.values, voff, Lrow, rc[qi].col, ne, rc[qi].nj, co, g, t);
           zero_tiles<NT>(co);
           face_contract(2, 4, co);
-          store_block<NT, false>(a.values, voff, Lrow, ns->col[qb], ne, ns->nj[qb], co, g, t);
+          store_block<NT, false>(a.values, voff, Lrow, rc[qb].col, ne, rc[qb].nj, co, g, t);
           __syncwarp();
           qi = qb + 1;
           continue;
         }
         // ---- general interface: every face, every sub-facet, rounds of 16 points
-        const int32_t j = ns->j[qi];
-        const int pj = ns->pj[qi];
+        const int32_t j = rc[qi].j;
+        const int pj = rc[qi].pj;
         const BoxConst<DIM> bo = load_box<DIM>(a.erec, j);
         const int order = 2 * max(pe, pj) + a.prm.quad_increment;
         const int r0 = R.face_offset[order], nq = R.face_count[order];
-        const int fend = ns->fb[qi];
-        for (int f = ns->fa[qi]; f < fend; ++f) {
+        const int fend = rc[qi].fb;
+        for (int f = rc[qi].fa; f < fend; ++f) {
           int side, info;
           double sig;
           double nrm[3] = {0.0, 0.0, 0.0};
           int64_t row0;
           int nrows;
-          if (f == ns->fa[qi]) {
-            info = ns->info[qi];
+          if (f == rc[qi].fa) {
+            info = rc[qi].info;
             side = info & 1;
-            sig = ns->sig[qi];
+            sig = rc[qi].sig;
 #pragma unroll
-            for (int i = 0; i < DIM; ++i) nrm[i] = ns->nrm[i][qi];
-            row0 = ns->row0[qi];
+            for (int i = 0; i < DIM; ++i) nrm[i] = rc[qi].nrm[i];
+            row0 = rc[qi].row0;
           } else {
             side = m.face_owner[f] == e ? 0 : 1;
             info = side | ((cf.has_adv() && a.flow[f] == side) ? 2 : 0);
@@ -703,7 +677,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
             __syncwarp();
           }
         }
-        store_block<NT, false>(a.values, voff, Lrow, ns->col[qi], ne, ns->nj[qi], co, g, t);
+        store_block<NT, false>(a.values, voff, Lrow, rc[qi].col, ne, rc[qi].nj, co, g, t);
         ++qi;
       }
       __syncwarp();

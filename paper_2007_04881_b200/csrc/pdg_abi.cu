@@ -137,6 +137,8 @@ static cudaError_t launch_tabulate(int P, const pdg_basis& B, int32_t el, const 
 
 using namespace pdg;
 
+static_assert(sizeof(pdg_iface_rec) == 64, "pdg_iface_rec is a 64-byte record");
+
 extern "C" int pdg_abi_version(void) { return PDG_ABI_VERSION; }
 
 extern "C" int64_t pdg_launch_count(void) { return (int64_t)g_launches.load(); }
@@ -154,6 +156,7 @@ extern "C" int pdg_assemble(const pdg_mesh* mesh, const pdg_basis* basis, const 
     if (!rules || !rules->sqrt_weights || !params || !pattern || !frames || !sigma || !face_flow || !values || !rhs)
       return fail(PDG_ERR_INVALID, "null argument");
     if (write_col_idx && !pattern->col_idx) return fail(PDG_ERR_INVALID, "col_idx not allocated");
+    if (!pattern->nbr_rec) return fail(PDG_ERR_INVALID, "interface records missing (pdg_iface_records)");
     const KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values,
                                write_col_idx, rhs, err_flags, 0);
     const bool sym = symmetric_accumulation(*coeffs);

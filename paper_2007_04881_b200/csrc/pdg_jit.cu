@@ -285,6 +285,7 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     if (!policy_source || !rules || !rules->sqrt_weights || !params || !pattern || !frames || !sigma || !face_flow || !values || !rhs)
       return fail(PDG_ERR_INVALID, "null argument");
     if (write_col_idx && !pattern->col_idx) return fail(PDG_ERR_INVALID, "col_idx not allocated");
+    if (!pattern->nbr_rec) return fail(PDG_ERR_INVALID, "interface records missing (pdg_iface_records)");
     JitKernel k;
     const bool sym = symmetric_accumulation(*coeffs);
     const bool ws = jit_ws();
