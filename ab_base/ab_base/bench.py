@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""fp64 SIPG assembly benchmark (BASELINE.json metric: assembly elements/s and
+wall ms at 1/2/4/8 B200, next to the host-CPU reference path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
+
+One step = one full assembly of the workload's rows on each rank: index
+phase (adjacency, row offsets), face pre-pass (sigma, flow side) and the fused
+element kernel (values + col_idx + RHS), with the mesh resident in HBM.
+Multi-GPU (torchrun): elements are split into contiguous, cost-balanced row
+ranges, one per rank; there is no collective on the assembly path (strong
+scaling of the fixed mesh); timing is the max over ranks of CUDA-event time.
+``e2e`` re-runs the step through the public plan API with the mesh copied
+from pinned host memory and the assembled CSR + RHS copied back every step.
+``--impl reference`` times the CPU restatement of polydg's path (oracle/,
+all host cores) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 SIPG assembly elements/s"
+UNIT = "elements/s"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--degree", type=int, default=None, help="override the workload degree")
+    ap.add_argument("--n", type=int, default=None, help="override the workload size")
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / baseline)")
+    return ap.parse_args()
+
+
+def workload(args):
+    from dataclasses import replace
+
+    from paper_2007_04881_b200.problems import WORKLOADS
+
+    w = WORKLOADS[args.config]
+    if args.degree is not None:
+        w = replace(w, degree=args.degree)
+    if args.n is not None:
+        w = replace(w, n=args.n)
+    return w
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling during the timed region (NVML)."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period: float = 0.1):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def fp64_peak():
+    """Measured FP64 (DMMA/DFMA) peak, TFLOP/s: profiles/fp64_peaks_r01.json
+    (MEASURED_PEAKS.json carries no fp64 figure)."""
+    p = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(max(d["dmma_m8n8k4_acc4_tflops"], d["dfma_tflops"])), "profiles/fp64_peaks_r01.json (measured)"
+    except Exception:
+        return 37.0, "B200 datasheet fallback"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json (measured)"
+    except Exception:
+        return 6650.0, "B200_PROFILING.md fallback"
+
+
+def ncu_traffic(config, n_elements):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the element kernel from
+    the committed ncu --set full capture (profiles/ncu_element_kernel.json),
+    per launch of this workload: the capture's bytes per element x elements
+    (the capture runs a smaller mesh of the same generator and degree)."""
+    p = os.path.join(ROOT, "profiles", "ncu_element_kernel.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d[config]["dram_bytes_per_element"]) * n_elements
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle restatement of polydg on all host cores)
+# ---------------------------------------------------------------------------
+
+class CpuReference:
+    """The oracle (plain-numpy port of polydg's assemble_approach2 path) on a
+    bounded sample: a sub-scale mesh from the same generator, coefficients and
+    degree, run with fork workers on all host cores.  Its elements/s is
+    rate-extrapolated to the full workload."""
+
+    def __init__(self, w, per_core: int = 150):
+        from dataclasses import replace
+
+        from oracle import sipg as oracle
+        from paper_2007_04881_b200 import build_basis, classify_boundary_faces
+        from paper_2007_04881_b200.problems import build_mesh, coefficients
+
+        self.oracle = oracle
+        self.cores = oracle.host_cores()
+        if w.dim == 2:
+            sw = replace(w, n=max(256, min(w.n, per_core * self.cores)))
+        else:
+            sw = replace(w, n=12, k=max(300, min(w.k, per_core * self.cores // 2)))
+        self.pm = build_mesh(sw)
+        self.coeffs = coefficients(w.coeffs, w.dim)
+        classify_boundary_faces(self.pm, self.coeffs)
+        self.specs = build_basis(self.pm, w.degree)
+        self.w = w
+
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        self.oracle.assemble(self.pm, self.coeffs, self.specs, workers=self.cores)
+        return time.perf_counter() - t0
+
+    def sample(self, dt) -> str:
+        kind = "Voronoi" if self.w.dim == 2 else "agglomerated Kuhn"
+        return (f"{self.pm.n_elements} elements of the same {kind} generator (p={self.w.degree}, "
+                f"{self.w.coeffs}); oracle/ numpy port of polydg assemble_approach2 with "
+                f"{self.cores} fork workers, {dt:.2f} s per assembly; elements/s rate-extrapolated "
+                f"to the {self.w.name} workload")
+
+
+def cpu_reference_rate(w, min_seconds=10.0):
+    ref = CpuReference(w)
+    total, n = 0.0, 0
+    while total < min_seconds or n < 1:
+        total += ref.step()
+        n += 1
+    dt = total / n
+    return ref.pm.n_elements / dt, ref.cores, ref.sample(dt), dt
+
+
+def run_reference(args, w, rank):
+    if rank != 0:
+        return  # rank 0 alone runs the CPU arm
+    ref = CpuReference(w)
+    for _ in range(args.warmup):
+        ref.step()
+    times = [ref.step() for _ in range(args.steps)]
+    dt = float(statistics.median(times))
+    value = ref.pm.n_elements / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": w.description, "name": w.name, "degree": w.degree,
+                                        "sample_elements": ref.pm.n_elements},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.cores, "kind": "port",
+                         "sample": ref.sample(dt)},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, w, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_04881_b200 import _lib, build_basis, classify_boundary_faces
+    from paper_2007_04881_b200.assembly import AssemblyConfig, HostIO, SipgPlan
+    from paper_2007_04881_b200.distribute import contiguous_partition, quadrature_cost_weights
+    from paper_2007_04881_b200.problems import cached_mesh, coefficients
+    from paper_2007_04881_b200.roofline import assembly_work
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        # rank 0 builds (or loads) the mesh first so the others hit the cache
+        if rank == 0:
+            t0 = time.perf_counter()
+            pm = cached_mesh(w)
+            mesh_s = time.perf_counter() - t0
+        dist.barrier()
+        if rank != 0:
+            t0 = time.perf_counter()
+            pm = cached_mesh(w)
+            mesh_s = time.perf_counter() - t0
+    else:
+        t0 = time.perf_counter()
+        pm = cached_mesh(w)
+        mesh_s = time.perf_counter() - t0
+    coeffs = coefficients(w.coeffs, w.dim)
+    classify_boundary_faces(pm, coeffs)
+    specs = build_basis(pm, w.degree)
+    cfg = AssemblyConfig()
+    rows = None
+    if world > 1:
+        part = contiguous_partition(pm, world, quadrature_cost_weights(pm, specs))
+        rows = part.owned[rank]
+    stream = torch.cuda.Stream(dev)
+    plan = SipgPlan(pm, coeffs, specs, cfg, row_elements=rows, device=dev, stream=stream)
+    work = assembly_work(plan)
+    lib = _lib.load()
+
+    # warm-up (first run also validates the device error flags)
+    for i in range(max(args.warmup, 1)):
+        plan.run()
+    plan.check_flags()
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_stop = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = lib.pdg_launch_count()
+    with ClockSampler(local_rank) as clk:
+        t_start.record(stream)
+        for k in range(K):
+            plan.run(evs[k])
+        t_stop.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = int(lib.pdg_launch_count() - l0)
+    ms = t_start.elapsed_time(t_stop) / K
+    ms_index = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    ms_pre = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    ms_el = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    plan.check_flags()
+
+    # end to end through the plan API with host buffers
+    e2e_ms, h2d, d2h = None, 0, 0
+    if not args.no_e2e and not args.profile and args.e2e_steps > 0:
+        io = HostIO(plan)
+        h2d, d2h = io.h2d_bytes, io.d2h_bytes
+        io.upload(); plan.run(); io.download()
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            io.upload()
+            plan.run()
+            io.download()
+        e1.record(stream)
+        stream.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        del io
+
+    def allmax(x):
+        if world == 1 or x is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    ms_max = allmax(ms)
+    e2e_max = allmax(e2e_ms)
+    el_ms_max = allmax(ms_el)
+    h2d_tot, d2h_tot = allsum(h2d), allsum(d2h)
+    launches_tot = allsum(launches / K)
+    n_el = pm.n_elements
+    if rank != 0:
+        return
+    peak, peak_src = fp64_peak()
+    hbm, hbm_src = hbm_peak()
+    achieved = work["flops"] / (ms_el * 1e-3) / 1e12
+    gbs = work["bytes"] / (ms_el * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": n_el / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated mesh; analytic coefficients)",
+        "config": {"workload": w.description, "name": w.name, "elements": n_el, "degree": w.degree,
+                   "dofs": int(plan.dof.n_dofs), "nnz": int(plan.nnz) if world == 1 else None,
+                   "parallelism": f"row-partitioned x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs+outputs >> 126 MB L2 (CSR written fresh each step), no flush needed"
+                   if plan.nnz * 16 > 4e8 else "small workload: L2-resident",
+                   "mesh_build_s": round(mesh_s, 1)},
+        "phases_ms": {"index": ms_index, "prepass": ms_pre, "element_kernel": ms_el},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(w.name, n_el),
+                     "kernel": "assemble_elements (fused volume+face+boundary, DMMA f64)",
+                     "algorithmic_flops_per_launch": work["flops"],
+                     "algorithmic_bytes_per_launch": work["bytes"],
+                     "hbm_achieved_gbs": gbs, "hbm_peak_gbs": hbm, "hbm_frac": gbs / hbm,
+                     "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "gpu_launches": int(round(launches_tot * K)),
+        "gpu_launches_per_step": launches_tot,
+    }
+    if e2e_max is not None:
+        line["e2e"] = {"value": n_el / (e2e_max * 1e-3), "unit": UNIT, "ms_per_step": e2e_max,
+                       "h2d_bytes_per_step": int(h2d_tot), "d2h_bytes_per_step": int(d2h_tot)}
+    if world == 1 and not args.no_cpu_baseline and not args.profile:
+        rate, cores, sample, _ = cpu_reference_rate(w)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    w = workload(args)
+    if args.impl == "reference":
+        run_reference(args, w, rank)  # CPU only; ranks != 0 exit without work
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, w, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,63 @@
+"""B200-native fp64 SIPG assembly on polytopic meshes (arXiv 2007.04881).
+
+Drop-in for polydg's Approach-2 assembly path: same entry points and
+containers, computed by hand-written sm_100a kernels in ``libpdg.so``
+(C ABI: ``include/pdg.h``).  See DESIGN.md.
+"""
+
+from .basis import BasisSpec, Family, SpecList, build_basis, num_basis
+from .mesh import (
+    BOUNDARY,
+    BoundaryTag,
+    FlatMesh,
+    MeshError,
+    PolytopicMesh,
+    SimplicialMesh,
+    agglomerate,
+    identity_agglomeration,
+)
+from .model import (
+    ClassificationError,
+    PdeCoefficients,
+    PenaltyConfig,
+    ScalarField,
+    TensorField,
+    VectorField,
+    classify_boundary_faces,
+    constant_scalar,
+    constant_tensor,
+    constant_vector,
+    isotropic_diffusion,
+    scalar_diffusion,
+)
+from .quadrature import QuadratureError
+from .assembly import (
+    AssemblyConfig,
+    AssemblyError,
+    AssemblyStats,
+    BlockPattern,
+    CSRMatrix,
+    DofMap,
+    KernelTiming,
+    PatternMissError,
+    SipgPlan,
+    assemble_approach1,
+    assemble_approach2,
+    assemble_device,
+    build_block_pattern,
+    element_kernel,
+)
+from .distribute import (
+    PartialMatrix,
+    Partition,
+    PartitionError,
+    assemble_partition,
+    contiguous_partition,
+    gather_and_verify,
+    gather_load,
+    partition_from_map,
+    quadrature_cost_weights,
+)
+
+__all__ = [n for n in dir() if not n.startswith("_")]
+__version__ = "0.1.0"

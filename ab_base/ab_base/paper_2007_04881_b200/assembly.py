@@ -1,0 +1,848 @@
+"""Drop-in Approach-2 assembly on the B200 engine.
+
+Public surface mirrors polydg ``assembly.py`` for the hot path:
+
+* ``assemble_approach2(mesh, coeffs, specs, config)`` -> ``(CSRMatrix, rhs,
+  AssemblyStats, BlockPattern)`` (polydg ``assembly.py:1090-1099``);
+* ``assemble_approach1`` -> ``(CSRMatrix, rhs, AssemblyStats)`` -- same device
+  engine (polydg's Approach 1 produces the same CSR within 1e-12);
+* ``build_block_pattern(mesh, specs, row_elements=None)``;
+* ``element_kernel`` (unit-level entry point);
+* ``assemble_device(...)`` -- the device-resident variant (CSR stays in HBM)
+  used by the benchmark and by million-element meshes.
+
+Everything numeric runs in ``libpdg.so``; this module only flattens inputs,
+allocates device buffers (PyTorch is used for device memory and streams) and
+maps device error flags to polydg's exception classes.  No CPU fallback.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+import warnings
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .basis import family_name, num_basis, spec_arrays
+from .mesh import BOUNDARY, TAG_CODE, FlatMesh, MeshError, flat_of
+from .model import ClassificationError, PenaltyConfig, compile_coeffs, policy_source
+from .quadrature import QuadratureError, RuleTable
+
+KERNEL_NAMES = ("element", "interior", "dirichlet", "inflow", "neumann_outflow")
+
+
+class AssemblyError(RuntimeError):
+    pass
+
+
+class PatternMissError(AssemblyError):
+    """A (row, col) block absent from the sparsity pattern was addressed."""
+
+
+# ---------------------------------------------------------------------------
+# polydg-compatible containers (assembly.py:64-155, 209-272, 345-391)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DofMap:
+    offsets: np.ndarray
+
+    @classmethod
+    def from_specs(cls, specs) -> "DofMap":
+        deg, boxes, fam = spec_arrays(specs)
+        d = boxes.shape[2]
+        counts = _num_basis_vec(deg, d, fam)
+        off = np.zeros(len(deg) + 1, dtype=np.int64)
+        np.cumsum(counts, out=off[1:])
+        return cls(off)
+
+    @property
+    def n_dofs(self) -> int:
+        return int(self.offsets[-1])
+
+    @property
+    def n_elements(self) -> int:
+        return self.offsets.shape[0] - 1
+
+    def count(self, element: int) -> int:
+        return int(self.offsets[element + 1] - self.offsets[element])
+
+    def start(self, element: int) -> int:
+        return int(self.offsets[element])
+
+
+def _num_basis_vec(degrees: np.ndarray, d: int, family) -> np.ndarray:
+    table = {int(p): num_basis(int(p), d, family) for p in np.unique(degrees)}
+    out = np.empty(degrees.shape[0], np.int64)
+    for p, n in table.items():
+        out[degrees == p] = n
+    return out
+
+
+@dataclass
+class CSRMatrix:
+    n_rows: int
+    n_cols: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.shape[0])
+
+    def validate(self) -> None:
+        if self.row_ptr.shape != (self.n_rows + 1,):
+            raise AssemblyError("row_ptr has wrong length")
+        if np.any(np.diff(self.row_ptr) < 0) or self.row_ptr[-1] != self.nnz:
+            raise AssemblyError("row_ptr is not a nondecreasing nnz prefix")
+        if self.nnz == 0:
+            return
+        if self.col_idx.min() < 0 or self.col_idx.max() >= self.n_cols:
+            raise AssemblyError("column index out of range")
+        first = np.zeros(self.nnz, bool)
+        first[self.row_ptr[:-1][self.row_ptr[:-1] < self.nnz]] = True
+        bad = np.flatnonzero((np.diff(self.col_idx) <= 0) & ~first[1:])
+        if bad.size:
+            r = int(np.searchsorted(self.row_ptr, bad[0] + 1, "right") - 1)
+            raise AssemblyError(f"row {r} columns not strictly increasing/in range")
+
+    def to_scipy(self):
+        from scipy.sparse import csr_matrix
+
+        return csr_matrix((self.values, self.col_idx, self.row_ptr), shape=(self.n_rows, self.n_cols))
+
+    def to_dense(self) -> np.ndarray:
+        return self.to_scipy().toarray()
+
+    def max_relative_difference(self, other: "CSRMatrix", floor_rel: float = 1e-3) -> float:
+        """polydg ``CSRMatrix.max_relative_difference`` (assembly.py:133-155)."""
+        if (self.n_rows != other.n_rows or self.n_cols != other.n_cols
+                or not np.array_equal(self.row_ptr, other.row_ptr)
+                or not np.array_equal(self.col_idx, other.col_idx)):
+            raise AssemblyError("sparsity patterns differ")
+        if self.nnz == 0:
+            return 0.0
+        a, b = np.abs(self.values), np.abs(other.values)
+        scale = max(a.max(), b.max(), 1e-300)
+        denom = np.maximum(np.maximum(a, b), floor_rel * scale)
+        return float(np.max(np.abs(self.values - other.values) / denom))
+
+
+@dataclass
+class BlockPattern:
+    """CSR skeleton with one dense block per adjacent element pair."""
+
+    dof_map: DofMap
+    row_elements: np.ndarray
+    neighbors: list
+    col_starts: list
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    global_rows: np.ndarray
+    _row_pos: dict = field(repr=False, default_factory=dict)
+
+    def __post_init__(self):
+        self._row_pos = {int(e): k for k, e in enumerate(self.row_elements)}
+        counts = np.diff(self.dof_map.offsets)[self.row_elements]
+        self._row_offsets = np.zeros(len(counts) + 1, dtype=np.int64)
+        np.cumsum(counts, out=self._row_offsets[1:])
+
+    @property
+    def n_local_rows(self) -> int:
+        return int(self.row_ptr.shape[0] - 1)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.shape[0])
+
+    def local_block_start(self, element: int) -> int:
+        return self._row_pos[element]
+
+    def block_slots(self, row_element: int, col_element: int) -> np.ndarray:
+        local = self._row_pos.get(row_element)
+        if local is None:
+            raise PatternMissError(f"element {row_element} owns no rows here")
+        nbrs = self.neighbors[local]
+        pos = int(np.searchsorted(nbrs, col_element))
+        if pos >= nbrs.shape[0] or nbrs[pos] != col_element:
+            raise PatternMissError(f"block ({row_element}, {col_element}) missing from pattern")
+        ni = self.dof_map.count(row_element)
+        nj = self.dof_map.count(col_element)
+        row0 = self._row_offsets[local]
+        base = self.row_ptr[row0: row0 + ni] + self.col_starts[local][pos]
+        return base[:, None] + np.arange(nj, dtype=np.int64)[None, :]
+
+    def empty_matrix(self) -> CSRMatrix:
+        return CSRMatrix(self.n_local_rows, self.dof_map.n_dofs, self.row_ptr.copy(),
+                         self.col_idx.copy(), np.zeros(self.nnz))
+
+
+@dataclass
+class AssemblyConfig:
+    """polydg ``AssemblyConfig`` (assembly.py:345-357).  ``n_workers``,
+    ``mode`` and ``chunk_size`` are accepted for compatibility: the device
+    engine has exactly one writer per value slot, so both modes give the same
+    bitwise-deterministic matrix."""
+
+    quad_increment: int = 2
+    penalty: PenaltyConfig = field(default_factory=PenaltyConfig)
+    n_workers: int = 1
+    mode: str = "deterministic"
+    chunk_size: int = 256
+
+    def __post_init__(self):
+        if self.mode not in ("deterministic", "atomic"):
+            raise ValueError(f"unknown accumulation mode {self.mode!r}")
+        if self.n_workers < 1:
+            raise ValueError("n_workers must be >= 1")
+
+
+@dataclass
+class KernelTiming:
+    kernel: str
+    work_items: int = 0
+    seconds: float = 0.0
+    nnz_written: int = 0
+
+
+@dataclass
+class AssemblyStats:
+    kernels: dict
+    index_seconds: float = 0.0
+    kernel_wall_seconds: float = 0.0
+    total_seconds: float = 0.0
+    triplet_count: int = 0
+    nnz: int = 0
+    device_ms: dict = field(default_factory=dict)
+
+    @property
+    def duplicate_ratio(self) -> float:
+        return self.triplet_count / self.nnz if self.nnz else 0.0
+
+    def to_csv(self) -> str:
+        lines = ["kernel,work_items,seconds,nnz_written"]
+        for name in KERNEL_NAMES:
+            k = self.kernels[name]
+            lines.append(f"{k.kernel},{k.work_items},{k.seconds:.6g},{k.nnz_written}")
+        total_items = sum(k.work_items for k in self.kernels.values())
+        lines.append(f"indices,{self.triplet_count},{self.index_seconds:.6g},{self.nnz}")
+        lines.append(f"total,{total_items},{self.total_seconds:.6g},{self.nnz}")
+        return "\n".join(lines) + "\n"
+
+
+# ---------------------------------------------------------------------------
+# device residency
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _require_cuda(device):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise _lib.EngineUnavailable("no CUDA device: the SIPG engine has no CPU fallback")
+    return torch.device(device if device is not None else "cuda")
+
+
+_MESH_FIELDS = (
+    ("vertices", "vertices"), ("simplices", "simplices"), ("simplex_volumes", "simplex_volumes"),
+    ("elem_ptr", "elem_ptr"), ("elem_simplices", "elem_simplices"), ("elem_volumes", "elem_volumes"),
+    ("face_owner", "face_owner"), ("face_neighbor", "face_neighbor"), ("face_tag", "face_tag"),
+    ("face_normal", "face_normal"), ("face_measure", "face_measure"), ("face_ptr", "face_ptr"),
+    ("facet_vertices", "facet_vertices"), ("facet_owner_simplex", "facet_owner_simplex"),
+    ("facet_neighbor_simplex", "facet_neighbor_simplex"), ("iface_owner", "iface_owner"),
+    ("iface_neighbor", "iface_neighbor"), ("iface_ptr", "iface_ptr"),
+    ("iface_faces", "iface_faces"), ("elem_bface_ptr", "elem_bface_ptr"),
+    ("elem_bfaces", "elem_bfaces"),
+)
+
+
+class DeviceMesh:
+    """A FlatMesh resident in HBM (+ the ``pdg_mesh`` descriptor)."""
+
+    def __init__(self, flat: FlatMesh, device=None, stream=None):
+        torch = _torch()
+        self.device = _require_cuda(device)
+        self.flat = flat
+        self.t = {}
+        for attr, _ in _MESH_FIELDS:
+            arr = np.ascontiguousarray(getattr(flat, attr))
+            if arr.size == 0:
+                arr = np.zeros(1, dtype=arr.dtype)
+            self.t[attr] = torch.from_numpy(arr).to(self.device, non_blocking=False)
+        self.h2d_bytes = sum(int(getattr(flat, a).nbytes) for a, _ in _MESH_FIELDS)
+        s = _lib.Mesh()
+        s.dim = flat.dim
+        s.n_vertices, s.n_simplices, s.n_elements = flat.n_vertices, flat.n_simplices, flat.n_elements
+        s.n_faces, s.n_facets, s.n_interfaces = flat.n_faces, flat.n_facets, flat.n_interfaces
+        for attr, cname in _MESH_FIELDS:
+            setattr(s, cname, _lib.ptr(self.t[attr]))
+        self.struct = s
+        self._tags = flat.face_tag.copy()
+
+    def refresh_tags(self):
+        """Re-upload face tags if classification changed them since upload."""
+        if not np.array_equal(self._tags, self.flat.face_tag):
+            torch = _torch()
+            src = self.flat.face_tag if self.flat.face_tag.size else np.zeros(1, np.int8)
+            self.t["face_tag"].copy_(torch.from_numpy(np.ascontiguousarray(src)))
+            self._tags = self.flat.face_tag.copy()
+
+
+def device_mesh(mesh, device=None) -> DeviceMesh:
+    """Cached DeviceMesh of a mesh object (this package's meshes keep it)."""
+    flat = flat_of(mesh)
+    cache = getattr(flat, "_device_cache", None)
+    if cache is not None and cache.device == _require_cuda(device):
+        cache.refresh_tags()
+        return cache
+    dm = DeviceMesh(flat, device)
+    try:
+        object.__setattr__(flat, "_device_cache", dm)
+    except Exception:
+        pass
+    return dm
+
+
+class DeviceRules:
+    def __init__(self, dim, vol_orders, face_orders, device):
+        torch = _torch()
+        table = RuleTable(dim, vol_orders, face_orders)
+        mo = max(list(table.vol) + list(table.face) + [2])
+        vo, vn, fo, fn = table.lookup_arrays(mo)
+        self.t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(device)
+                  for k, v in (("points", table.points if table.points.size else np.zeros((1, 3))),
+                               ("weights", table.weights if table.weights.size else np.zeros(1)),
+                               ("sqrt_weights", np.sqrt(table.weights) if table.weights.size else np.zeros(1)),
+                               ("vo", vo), ("vn", vn), ("fo", fo), ("fn", fn))}
+        r = _lib.Rules()
+        r.max_order = mo
+        r.points, r.weights = _lib.ptr(self.t["points"]), _lib.ptr(self.t["weights"])
+        r.vol_offset, r.vol_count = _lib.ptr(self.t["vo"]), _lib.ptr(self.t["vn"])
+        r.face_offset, r.face_count = _lib.ptr(self.t["fo"]), _lib.ptr(self.t["fn"])
+        r.sqrt_weights = _lib.ptr(self.t["sqrt_weights"])
+        self.struct = r
+
+
+def _raise_flags(flags: int):
+    if flags & _lib.FLAG_UNCLASSIFIED:
+        raise AssemblyError("a boundary face is unclassified; run classify_boundary_faces")
+    if flags & (_lib.FLAG_DEGENERATE_SIMPLEX):
+        raise QuadratureError("degenerate simplex in quadrature map")
+    if flags & (_lib.FLAG_DEGENERATE_FACET):
+        raise QuadratureError("degenerate sub-simplex in face quadrature map")
+    if flags & _lib.FLAG_STRADDLE:
+        raise ClassificationError(
+            "advection flux changes sign across a face; refine the mesh so faces do not "
+            "straddle the inflow/outflow transition")
+    if flags & _lib.FLAG_NO_ADJACENT_SIMPLEX:
+        raise MeshError("no subdivision simplex adjacent to the face")
+    if flags:
+        raise RuntimeError(f"device error flags 0x{flags:x}")
+
+
+# ---------------------------------------------------------------------------
+# the assembly plan: all device buffers of one (mesh, basis, coeffs, rows)
+# ---------------------------------------------------------------------------
+
+class SipgPlan:
+    """Device buffers + descriptors for repeated assembly of one problem.
+
+    ``run()`` enqueues the whole path on one stream -- index phase
+    (adjacency, row offsets), face pre-pass (sigma, flow side) and the fused
+    element kernel (values + col_idx + RHS) -- without any host
+    synchronisation, so it can be timed with CUDA events or captured in a
+    CUDA graph.  Construction performs the one size query (nnz) polydg also
+    needs before it can allocate the CSR.
+    """
+
+    def __init__(self, mesh, coeffs, specs, config: Optional[AssemblyConfig] = None,
+                 row_elements=None, device=None, stream=None, jit: bool = True):
+        import ctypes as C
+
+        torch = _torch()
+        self.lib = _lib.load()
+        config = config or AssemblyConfig()
+        self.config = config
+        self.dm = device_mesh(mesh, device)
+        dev = self.dm.device
+        self.device = dev
+        flat = self.dm.flat
+        self.flat = flat
+        d = flat.dim
+        deg, boxes, fam = spec_arrays(specs)
+        if family_name(fam) != "P":
+            raise NotImplementedError("the device engine implements family P (space-time PQ is out of scope)")
+        if deg.shape[0] != flat.n_elements:
+            raise AssemblyError("one BasisSpec per element required")
+        if boxes.shape[1:] != (2, d):
+            raise ValueError("spec boxes do not match the mesh dimension")
+        pmax = int(deg.max()) if deg.size else 0
+        if pmax > _lib.MAX_DEGREE[d]:
+            raise NotImplementedError(
+                f"degree {pmax} exceeds the compiled device range (p <= {_lib.MAX_DEGREE[d]} in {d}D)")
+        self.degrees = deg
+        self.dof = DofMap(np.concatenate([[0], np.cumsum(_num_basis_vec(deg, d, fam))]).astype(np.int64))
+        inc = int(config.quad_increment)
+        pen = config.penalty
+        self.coverable = None if pen.coverable is None else np.asarray(pen.coverable, bool)
+
+        self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        self.t = {"degree": T(deg.astype(np.int32)), "box": T(boxes), "dof": T(self.dof.offsets)}
+        b = _lib.Basis()
+        b.max_degree = pmax
+        b.degree, b.box, b.dof_offset = (_lib.ptr(self.t["degree"]), _lib.ptr(self.t["box"]),
+                                         _lib.ptr(self.t["dof"]))
+        self.basis = b
+
+        # rules: volume orders per degree present, face orders per max pair degree
+        uniq = np.unique(deg)
+        vol_orders = [2 * int(p) + inc for p in uniq]
+        face_orders = [2 * int(max(p, q)) + inc for p in uniq for q in uniq]
+        self.rules = DeviceRules(d, vol_orders, face_orders, dev)
+
+        self.cdesc = compile_coeffs(coeffs, d)
+        self.coeffs = _lib.coeffs_struct(self.cdesc)
+        self.jit_source = None
+        self.kernel_variant = "aot-interpreted"
+        if jit and os.environ.get("PDG_JIT", "1") != "0":
+            src = policy_source(coeffs, d).encode()
+            rc = self.lib.pdg_jit_prepare(C.byref(self.coeffs), src, d, pmax)
+            if rc == _lib.PDG_OK:
+                self.jit_source = src
+                self.kernel_variant = "nvrtc-specialised"
+            else:
+                warnings.warn("runtime specialisation unavailable, using the ahead-of-time kernel: "
+                              + self.lib.pdg_last_error().decode(errors="replace"))
+        prm = _lib.Params()
+        prm.quad_increment = inc
+        prm.include_gradient_terms = 1
+        prm.penalty_constant = float(pen.constant)
+        if os.environ.get("PDG_PLAIN_VOLUME") == "1":  # variant selection for experiments / tests
+            prm.options |= _lib.OPT_PLAIN_VOLUME
+        if self.coverable is not None:
+            self.t["coverable"] = T(self.coverable.astype(np.uint8))
+            prm.coverable = _lib.ptr(self.t["coverable"])
+        self.params = prm
+
+        # rows
+        nel = flat.n_elements
+        if row_elements is None:
+            self.row_elements = np.arange(nel, dtype=np.int64)
+            self.t["rows"] = None
+        else:
+            self.row_elements = np.unique(np.asarray(row_elements, dtype=np.int64))
+            self.t["rows"] = T(self.row_elements.astype(np.int32))
+        nr = self.row_elements.shape[0]
+        counts = np.diff(self.dof.offsets)
+        self.n_local_rows = int(counts[self.row_elements].sum())
+        z = lambda n, dt: torch.empty(max(int(n), 1), dtype=dt, device=dev)
+        i64, i32 = torch.int64, torch.int32
+        nadj = nel + 2 * flat.n_interfaces
+        self.t.update(nbr_ptr=z(nel + 1, i64), nbr_elem=z(nadj, i32), nbr_iface=z(nadj, i32),
+                      row_len=z(nr, i64), val_off=z(nr + 1, i64), row_off=z(nr + 1, i64),
+                      row_ptr=z(self.n_local_rows + 1, i64),
+                      nbr_rec=z(nadj * 8, torch.float64),  # pdg_iface_rec, 64 B per entry
+                      sigma=z(flat.n_faces, torch.float64), flow=z(flat.n_faces, torch.int8),
+                      abar=z(nel, torch.float64), flags=torch.zeros(1, dtype=torch.int32, device=dev))
+        W = 8 if d == 2 else 16
+        self.t.update(sframe=z(flat.n_simplices * W, torch.float64),
+                      fframe=z(flat.n_facets * W, torch.float64),
+                      erec=z(nel * W, torch.float64))
+        fr = _lib.Frames()
+        fr.simplex, fr.facet, fr.element = (_lib.ptr(self.t["sframe"]), _lib.ptr(self.t["fframe"]),
+                                            _lib.ptr(self.t["erec"]))
+        self.frames = fr
+        self.ws_bytes = int(self.lib.pdg_workspace_bytes(nel, flat.n_interfaces))
+        self.t["ws"] = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        pat = _lib.Pattern()
+        pat.n_row_elements = nr
+        pat.row_elements = _lib.ptr(self.t["rows"])
+        pat.nbr_ptr, pat.nbr_elem, pat.nbr_iface = (_lib.ptr(self.t["nbr_ptr"]),
+                                                    _lib.ptr(self.t["nbr_elem"]),
+                                                    _lib.ptr(self.t["nbr_iface"]))
+        pat.row_len, pat.elem_val_offset, pat.elem_row_offset = (
+            _lib.ptr(self.t["row_len"]), _lib.ptr(self.t["val_off"]), _lib.ptr(self.t["row_off"]))
+        pat.row_ptr = _lib.ptr(self.t["row_ptr"])
+        pat.nbr_rec = _lib.ptr(self.t["nbr_rec"])
+        self.pattern = pat
+
+        # size query (the one sync, like polydg's pattern build before values)
+        with torch.cuda.stream(self.stream):
+            self._index_phase(size_query=True)
+        self.t["col_idx"] = z(self.nnz, i64)
+        self.t["values"] = z(self.nnz, torch.float64)
+        self.t["rhs"] = torch.zeros(max(self.dof.n_dofs, 1), dtype=torch.float64, device=dev)
+        pat.col_idx = _lib.ptr(self.t["col_idx"])
+
+    # -- phases --------------------------------------------------------------
+    def _index_phase(self, size_query=False):
+        import ctypes as C
+
+        s = _lib.stream_ptr(self.stream)
+        lib = self.lib
+        _lib.check(lib.pdg_adjacency(C.byref(self.dm.struct), _lib.ptr(self.t["nbr_ptr"]),
+                                     _lib.ptr(self.t["nbr_elem"]), _lib.ptr(self.t["nbr_iface"]),
+                                     _lib.ptr(self.t["ws"]), self.ws_bytes, s))
+        nnz = C.c_int64(0)
+        _lib.check(lib.pdg_pattern_offsets(C.byref(self.dm.struct), C.byref(self.basis),
+                                           C.byref(self.pattern), self.n_local_rows,
+                                           C.byref(nnz) if size_query else None,
+                                           _lib.ptr(self.t["ws"]), self.ws_bytes, s))
+        if size_query:
+            self.nnz = int(nnz.value)
+
+    def _prepass(self):
+        import ctypes as C
+
+        _lib.check(self.lib.pdg_frames_build(C.byref(self.dm.struct), C.byref(self.basis),
+                                             C.byref(self.frames), _lib.ptr(self.t["flags"]),
+                                             _lib.stream_ptr(self.stream)))
+        _lib.check(self.lib.pdg_face_prepass(
+            C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs),
+            C.byref(self.rules.struct), C.byref(self.params), _lib.ptr(self.t["sigma"]),
+            _lib.ptr(self.t["flow"]), _lib.ptr(self.t["abar"]), _lib.ptr(self.t["flags"]),
+            _lib.stream_ptr(self.stream)))
+        _lib.check(self.lib.pdg_iface_records(
+            C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs),
+            C.byref(self.rules.struct), C.byref(self.params), C.byref(self.pattern),
+            _lib.ptr(self.t["sigma"]), _lib.ptr(self.t["flow"]), _lib.stream_ptr(self.stream)))
+
+    def _elements(self, write_col_idx=True):
+        import ctypes as C
+
+        tail = (C.byref(self.rules.struct), C.byref(self.params), C.byref(self.pattern),
+                C.byref(self.frames), _lib.ptr(self.t["sigma"]), _lib.ptr(self.t["flow"]),
+                _lib.ptr(self.t["values"]), 1 if write_col_idx else 0, _lib.ptr(self.t["rhs"]),
+                _lib.ptr(self.t["flags"]), _lib.stream_ptr(self.stream))
+        head = (C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs))
+        if self.jit_source is not None:
+            _lib.check(self.lib.pdg_assemble_jit(*head, self.jit_source, *tail))
+        else:
+            _lib.check(self.lib.pdg_assemble(*head, *tail))
+
+    def run(self, events=None):
+        """Enqueue index phase + pre-pass + element kernel; no host sync.
+        ``events``: optional list of 4 CUDA events recorded between phases."""
+        torch = _torch()
+        with torch.cuda.stream(self.stream):
+            if events:
+                events[0].record(self.stream)
+            self._index_phase()
+            if events:
+                events[1].record(self.stream)
+            self._prepass()
+            if events:
+                events[2].record(self.stream)
+            self._elements()
+            if events:
+                events[3].record(self.stream)
+
+    def check_flags(self):
+        self.stream.synchronize()
+        flags = int(self.t["flags"].item())
+        if flags & _lib.FLAG_NEG_DIFFUSION and not self.params.options & _lib.OPT_PLAIN_VOLUME:
+            # the symmetric sqrt(w a) volume table needs a(x) >= 0: re-run the
+            # assembly with the plain (w a dphi) dphi^T variant (same kernel family)
+            self.params.options |= _lib.OPT_PLAIN_VOLUME
+            self.t["flags"].zero_()
+            self.run()
+            self.stream.synchronize()
+            flags = int(self.t["flags"].item())
+        _raise_flags(flags & ~_lib.FLAG_NEG_DIFFUSION)
+
+    # -- results ----------------------------------------------------------------
+    @property
+    def values(self):
+        return self.t["values"][: self.nnz]
+
+    @property
+    def col_idx(self):
+        return self.t["col_idx"][: self.nnz]
+
+    @property
+    def row_ptr(self):
+        return self.t["row_ptr"][: self.n_local_rows + 1]
+
+    @property
+    def rhs(self):
+        return self.t["rhs"][: self.dof.n_dofs]
+
+    def to_csr(self) -> CSRMatrix:
+        return CSRMatrix(self.n_local_rows, self.dof.n_dofs, self.row_ptr.cpu().numpy(),
+                         self.col_idx.cpu().numpy(), self.values.cpu().numpy())
+
+    def block_pattern(self) -> BlockPattern:
+        ptr = self.t["nbr_ptr"].cpu().numpy()
+        nb = self.t["nbr_elem"][: int(ptr[-1])].cpu().numpy().astype(np.int64)
+        counts = np.diff(self.dof.offsets)
+        neighbors, col_starts, grows = [], [], []
+        for e in self.row_elements:
+            ns = nb[ptr[e]:ptr[e + 1]]
+            w = counts[ns]
+            st = np.zeros(ns.shape[0], np.int64)
+            np.cumsum(w[:-1], out=st[1:])
+            neighbors.append(ns)
+            col_starts.append(st)
+            grows.append(np.arange(self.dof.offsets[e], self.dof.offsets[e + 1]))
+        gr = np.concatenate(grows) if grows else np.zeros(0, np.int64)
+        return BlockPattern(self.dof, self.row_elements, neighbors, col_starts,
+                            self.row_ptr.cpu().numpy(), self.col_idx.cpu().numpy(), gr)
+
+    def work_stats(self) -> dict:
+        """polydg per-kernel work items / nnz_written (assembly.py:360-391)."""
+        f = self.flat
+        counts = np.diff(self.dof.offsets)
+        owned = np.zeros(f.n_elements, bool)
+        owned[self.row_elements] = True
+        nsim = np.diff(f.elem_ptr)
+        out = {k: KernelTiming(k) for k in KERNEL_NAMES}
+        out["element"].work_items = int(nsim[owned].sum())
+        out["element"].nnz_written = int((nsim * counts * counts)[owned].sum())
+        nfac = np.diff(f.face_ptr)
+        o, nb = f.face_owner, f.face_neighbor
+        inter = nb != BOUNDARY
+        no, nn = counts[o], counts[np.where(inter, nb, 0)]
+        oo = owned[o]
+        on = np.where(inter, owned[np.where(inter, nb, 0)], False)
+        both = inter & oo & on
+        one_o = inter & oo & ~on
+        one_n = inter & on & ~oo
+        per = np.zeros(f.n_faces, np.int64)
+        per[both] = ((no + nn) ** 2)[both]
+        per[one_o] = (no * (no + nn))[one_o]
+        per[one_n] = (nn * (no + nn))[one_n]
+        sel = both | one_o | one_n
+        out["interior"].work_items = int(nfac[sel].sum())
+        out["interior"].nnz_written = int((per * nfac)[sel].sum())
+        tg = f.face_tag
+        for name, codes in (("dirichlet", (TAG_CODE["dirichlet"],)),
+                            ("inflow", (TAG_CODE["inflow"],)),
+                            ("neumann_outflow", (TAG_CODE["neumann"], TAG_CODE["outflow"]))):
+            m = (~inter) & oo & np.isin(tg, codes)
+            out[name].work_items = int(nfac[m].sum())
+            if name != "neumann_outflow":
+                out[name].nnz_written = int((nfac * no * no)[m].sum())
+        return out
+
+
+class HostIO:
+    """Pinned-host staging for end-to-end runs of a plan: every ``upload()``
+    copies the mesh arrays host->device (the assembly inputs), every
+    ``download()`` moves the assembled CSR (row_ptr, col_idx, values) and the
+    RHS device->host through a pinned staging ring of ``chunk_bytes``.  The
+    bytes moved are the full result; only the host-side retention is bounded
+    (a 4M-element p=4 matrix is ~100 GB)."""
+
+    def __init__(self, plan: "SipgPlan", chunk_bytes: int = 1 << 30):
+        torch = _torch()
+        self.plan = plan
+        self.inputs = {}
+        for attr, _ in _MESH_FIELDS:
+            src = plan.dm.t[attr]
+            h = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+            h.copy_(src)
+            self.inputs[attr] = h
+        self.h2d_bytes = sum(int(t.numel() * t.element_size()) for t in self.inputs.values())
+        self.stage = torch.empty(chunk_bytes, dtype=torch.uint8, pin_memory=True)
+        outs = (plan.row_ptr, plan.col_idx, plan.values, plan.rhs)
+        self.d2h_bytes = sum(int(t.numel() * t.element_size()) for t in outs)
+
+    def upload(self):
+        torch = _torch()
+        with torch.cuda.stream(self.plan.stream):
+            for attr, h in self.inputs.items():
+                self.plan.dm.t[attr].copy_(h, non_blocking=True)
+
+    def download(self):
+        torch = _torch()
+        p = self.plan
+        cap = self.stage.numel()
+        with torch.cuda.stream(p.stream):
+            for t in (p.row_ptr, p.col_idx, p.values, p.rhs):
+                flat = t.reshape(-1).view(torch.uint8)
+                for a in range(0, flat.numel(), cap):
+                    b = min(a + cap, flat.numel())
+                    self.stage[: b - a].copy_(flat[a:b], non_blocking=True)
+
+
+@dataclass
+class DeviceAssembly:
+    """Device-resident result of one assembly (CSR in HBM)."""
+
+    plan: SipgPlan
+    stats: AssemblyStats
+
+    @property
+    def row_ptr(self):
+        return self.plan.row_ptr
+
+    @property
+    def col_idx(self):
+        return self.plan.col_idx
+
+    @property
+    def values(self):
+        return self.plan.values
+
+    @property
+    def rhs(self):
+        return self.plan.rhs
+
+    def to_csr(self) -> CSRMatrix:
+        return self.plan.to_csr()
+
+
+def assemble_device(mesh, coeffs, specs, config: Optional[AssemblyConfig] = None,
+                    row_elements=None, device=None, stream=None) -> DeviceAssembly:
+    """Assemble on the GPU and keep the CSR in HBM."""
+    torch = _torch()
+    t0 = time.perf_counter()
+    plan = SipgPlan(mesh, coeffs, specs, config, row_elements, device, stream)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    plan.run(ev)
+    plan.check_flags()
+    ms_index = ev[0].elapsed_time(ev[1])
+    ms_pre = ev[1].elapsed_time(ev[2])
+    ms_el = ev[2].elapsed_time(ev[3])
+    kern = plan.work_stats()
+    kern["element"].seconds = ms_el * 1e-3      # fused volume + face + boundary kernel
+    kern["interior"].seconds = ms_pre * 1e-3    # sigma / flow-side pre-pass
+    stats = AssemblyStats(
+        kernels=kern, index_seconds=ms_index * 1e-3,
+        kernel_wall_seconds=(ms_pre + ms_el) * 1e-3,
+        total_seconds=time.perf_counter() - t0,
+        triplet_count=sum(k.nnz_written for k in kern.values()), nnz=plan.nnz,
+        device_ms={"index": ms_index, "prepass": ms_pre, "element": ms_el})
+    return DeviceAssembly(plan, stats)
+
+
+# ---------------------------------------------------------------------------
+# polydg-compatible entry points
+# ---------------------------------------------------------------------------
+
+def _check_classified(mesh):
+    flat = flat_of(mesh)
+    bad = np.flatnonzero((flat.face_neighbor == BOUNDARY) & (flat.face_tag == TAG_CODE["interior"]))
+    if bad.size:
+        raise AssemblyError(f"boundary face {int(bad[0])} is unclassified; run classify_boundary_faces")
+
+
+def assemble_approach2(mesh, coeffs, specs, config: Optional[AssemblyConfig] = None):
+    """Preset-sparsity assembly on the B200 (polydg ``assembly.py:1090-1099``)."""
+    t0 = time.perf_counter()
+    _check_classified(mesh)
+    res = assemble_device(mesh, coeffs, specs, config)
+    plan = res.plan
+    matrix = plan.to_csr()
+    rhs = plan.rhs.cpu().numpy().copy()
+    pattern = plan.block_pattern()
+    res.stats.total_seconds = time.perf_counter() - t0
+    return matrix, rhs, res.stats, pattern
+
+
+def assemble_approach1(mesh, coeffs, specs, config: Optional[AssemblyConfig] = None):
+    """polydg's stage-and-sort path yields the same CSR (within 1e-12); on the
+    device both entry points run the preset-sparsity engine."""
+    matrix, rhs, stats, _ = assemble_approach2(mesh, coeffs, specs, config)
+    return matrix, rhs, stats
+
+
+def _assemble_approach2_rows(mesh, coeffs, specs, config, row_elements):
+    _check_classified(mesh)
+    res = assemble_device(mesh, coeffs, specs, config, row_elements=row_elements)
+    return res
+
+
+def build_block_pattern(mesh, specs, row_elements=None) -> BlockPattern:
+    """Block pattern on the device (polydg ``assembly.py:275-287``)."""
+    import ctypes as C
+
+    from .model import PdeCoefficients
+
+    plan = SipgPlan(mesh, PdeCoefficients(), specs, AssemblyConfig(), row_elements)
+    _lib.check(plan.lib.pdg_pattern_fill(C.byref(plan.dm.struct), C.byref(plan.basis),
+                                         C.byref(plan.pattern), _lib.stream_ptr(plan.stream)))
+    plan.stream.synchronize()
+    return plan.block_pattern()
+
+
+def element_kernel(mesh, element, coeffs, spec, quad_increment=2):
+    """Volume block and load of one element (polydg ``assembly.py:1139-1152``),
+    computed by the device element kernel (volume-only mode)."""
+    import ctypes as C
+
+    from .basis import BasisSpec
+
+    torch = _torch()
+    flat = flat_of(mesh)
+    nel = flat.n_elements
+    specs = [BasisSpec(spec.degree, spec.family, spec.box)] * nel
+    plan = _UnitPlan(mesh, coeffs, specs, quad_increment)
+    nb = num_basis(spec.degree, flat.dim)
+    ids = torch.tensor([int(element)], dtype=torch.int32, device=plan.device)
+    blocks = torch.zeros(nb * nb, dtype=torch.float64, device=plan.device)
+    loads = torch.zeros(nb, dtype=torch.float64, device=plan.device)
+    _lib.check(plan.lib.pdg_frames_build(C.byref(plan.dm.struct), C.byref(plan.basis),
+                                         C.byref(plan.frames), _lib.ptr(plan.flags),
+                                         _lib.stream_ptr(plan.stream)))
+    for _ in range(2):
+        _lib.check(plan.lib.pdg_element_blocks(
+            C.byref(plan.dm.struct), C.byref(plan.basis), C.byref(plan.coeffs),
+            C.byref(plan.rules.struct), C.byref(plan.params), C.byref(plan.frames), _lib.ptr(ids), 1,
+            _lib.ptr(blocks), _lib.ptr(loads), _lib.ptr(plan.flags), _lib.stream_ptr(plan.stream)))
+        plan.stream.synchronize()
+        flags = int(plan.flags.item())
+        if not flags & _lib.FLAG_NEG_DIFFUSION or plan.params.options & _lib.OPT_PLAIN_VOLUME:
+            break
+        plan.params.options |= _lib.OPT_PLAIN_VOLUME  # a(x) < 0: plain volume variant
+        plan.flags.zero_()
+    _raise_flags(flags & ~_lib.FLAG_NEG_DIFFUSION)
+    return blocks.cpu().numpy().reshape(nb, nb), loads.cpu().numpy()
+
+
+class _UnitPlan:
+    """Descriptors for the unit entry points (no pattern)."""
+
+    def __init__(self, mesh, coeffs, specs, quad_increment=2):
+        torch = _torch()
+        self.lib = _lib.load()
+        self.dm = device_mesh(mesh)
+        self.device = self.dm.device
+        d = self.dm.flat.dim
+        deg, boxes, fam = spec_arrays(specs)
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+        self.t = {"degree": T(deg.astype(np.int32)), "box": T(boxes),
+                  "dof": T(np.concatenate([[0], np.cumsum(_num_basis_vec(deg, d, fam))]).astype(np.int64))}
+        b = _lib.Basis()
+        b.max_degree = int(deg.max())
+        b.degree, b.box, b.dof_offset = (_lib.ptr(self.t["degree"]), _lib.ptr(self.t["box"]),
+                                         _lib.ptr(self.t["dof"]))
+        self.basis = b
+        uniq = np.unique(deg)
+        self.rules = DeviceRules(d, [2 * int(p) + quad_increment for p in uniq],
+                                 [2 * int(p) + quad_increment for p in uniq], self.device)
+        self.coeffs = _lib.coeffs_struct(compile_coeffs(coeffs, d))
+        self.params = _lib.Params()
+        self.params.quad_increment = quad_increment
+        self.params.include_gradient_terms = 1
+        self.params.penalty_constant = 10.0
+        self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        f = self.dm.flat
+        W = 8 if d == 2 else 16
+        mk = lambda n: torch.empty(max(int(n) * W, 1), dtype=torch.float64, device=self.device)
+        self.t.update(sframe=mk(f.n_simplices), fframe=mk(f.n_facets), erec=mk(f.n_elements))
+        fr = _lib.Frames()
+        fr.simplex, fr.facet, fr.element = (_lib.ptr(self.t["sframe"]), _lib.ptr(self.t["fframe"]),
+                                            _lib.ptr(self.t["erec"]))
+        self.frames = fr

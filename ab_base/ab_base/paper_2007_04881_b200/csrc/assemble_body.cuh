@@ -1,0 +1,824 @@
+// The element kernel body: one warp owns one row element and produces all of
+// its CSR rows and its RHS segment in a single pass.
+//
+//   volume    K_e  += sum_q w [ (A grad phi_j).grad phi_i + (b.grad phi_j) phi_i + c phi_j phi_i ]
+//                                                        (polydg assembly.py:396-415)
+//   faces     rows of e of the SIPG interior blocks     (assembly.py:418-463)
+//             with both traces evaluated here, so every value slot has exactly
+//             one writer (no atomics, no zero-fill pass, bitwise deterministic,
+//             and a row-partitioned run reproduces the one-sided cut-face
+//             semantics of assembly.py:685-696,778-788 for free)
+//   boundary  Dirichlet / inflow / Neumann terms         (assembly.py:466-512)
+//
+// Every term is a sum of rank-1 updates C += L R^T over "items" (one per
+// quadrature point and term), contracted with DMMA m8n8k4 (SASS DMMA.8x8x4):
+//   volume   ISO   L = w a dphi/dx_c,   R = dphi/dx_c              (c < d)
+//            FULL  L = w dphi/dx_c,     R = (A grad phi)_c
+//            b/c   L = w phi,           R = b.grad phi + c phi
+//   face     L1 = alpha V_a + beta F_a, L2 = beta V_a, with
+//            alpha = w sigma - s_a [e downwind] w b.n,  beta = -1/2 s_a w,
+//            diag  C_aa += L1 V_a^T + L2 F_a^T,  off  C_ab += L1 (-V_b)^T + L2 F_b^T
+//   (F = n_owner . A grad phi; derivation in DESIGN.md §3).
+//
+// Quadrature points are tabulated lane-parallel (one lane = one point) into a
+// per-warp shared-memory table laid out [row][function][slot] with a slot
+// stride = 4 (mod 16) doubles, so both the tabulation stores (consecutive
+// slots) and the DMMA fragment loads (8 functions x 4 slots) are bank-conflict
+// free.  Geometry arrives pre-mapped: per-simplex / per-facet affine frames
+// and per-element basis constants are produced once per assembly by
+// geometry_frames (pdg_prepass.cu), so a quadrature point costs one broadcast
+// load of its frame instead of three dependent gathers.
+//
+// The coefficient fields enter through a policy class CF: the ahead-of-time
+// library uses InterpCoef (bytecode interpreter over pdg_coeffs); the runtime
+// specialisation (pdg_jit.cu, NVRTC) passes a generated class whose fields are
+// inlined expressions and whose kind flags are compile-time constants.
+#pragma once
+
+#include "sipg_device.cuh"
+
+namespace pdg {
+
+// RHS partials of a lane live in registers when the basis has at most this
+// many functions, else in a lane-private shared-memory column (fewer
+// registers, more shared memory); the runtime specialisation sets it per
+// compile (pdg_jit.cu), the host layout (make_layout) must agree.
+#ifndef PDG_RHS_REGS_MAX
+#define PDG_RHS_REGS_MAX 20
+#endif
+
+// unroll factors of the k-step loops (tuning knobs, PDG_JIT_DEFINES)
+#define PDG_STR_(x) #x
+#define PDG_UNROLL(n) _Pragma(PDG_STR_(unroll n))
+#ifndef PDG_VOL_UNROLL
+#define PDG_VOL_UNROLL 1
+#endif
+#ifndef PDG_FACE_UNROLL
+#define PDG_FACE_UNROLL 1
+#endif
+
+constexpr int KF = 16;   // face slots per round
+constexpr int KFP = 20;  // face slot stride
+constexpr int NBR_WIN = 16;  // neighbour entries staged per window
+constexpr int FR_MAX = 32;   // simplex frames of one element kept in shared memory
+
+template <int DIM>
+struct Widths {
+  static constexpr int SF = DIM == 2 ? 8 : 16;  // simplex frame: v0, E (row-major), |det|
+  static constexpr int FF = DIM == 2 ? 8 : 16;  // facet frame: v0, E rows, sqrt(det(EE^T))
+  static constexpr int ER = DIM == 2 ? 8 : 16;  // element record: centre, 1/half, 1/sqrt(width)
+};
+
+struct AsmLayout {
+  int kv;            // volume slots per round (16 or 32)
+  int vrows;         // volume table rows
+  int warp_doubles;  // per-warp shared memory (doubles)
+  int buf_doubles;   // table part of it (scalars + staging follow)
+};
+
+struct KArgs {
+  pdg_mesh m;
+  pdg_basis B;
+  pdg_rules R;
+  pdg_params prm;
+  pdg_pattern pat;
+  const double* sigma;
+  const int8_t* flow;
+  const double* sframe;  // [n_simplices][SF], element order (elem_ptr indexing)
+  const double* fframe;  // [n_facets][FF]
+  const double* erec;    // [n_elements][ER]
+  double* values;
+  double* rhs;
+  uint32_t* flags;
+  int write_cols;
+  int mode;  // 0: CSR rows; 1: dense volume-only blocks (unit entry point)
+  AsmLayout lay;
+};
+
+template <int DIM, int P>
+struct Shape {
+  static constexpr int NB = binom(P + DIM, DIM);
+  static constexpr int NT = (NB + 7) / 8;
+  static constexpr int NBP = NT * 8;
+  static constexpr bool RHS_REGS = NB <= PDG_RHS_REGS_MAX;
+};
+
+// per-warp staging of the neighbour window -- after the scalars
+struct NbrStage {
+  double sig[NBR_WIN];     // penalty of the interface's first face
+  double nrm[3][NBR_WIN];  // its owner normal
+  int j[NBR_WIN], nj[NBR_WIN], col[NBR_WIN], fa[NBR_WIN], fb[NBR_WIN], pj[NBR_WIN];
+  int info[NBR_WIN];       // bit0 e is the neighbour side, bit1 e downwind, bit2 paired-round eligible
+  int row0[NBR_WIN];       // first sub-facet row of the first face
+};
+
+// Ahead-of-time coefficient policy: interprets the bytecode in pdg_coeffs.
+template <int DIM>
+struct InterpCoef {
+  const pdg_coeffs& C;
+  __device__ InterpCoef(const pdg_coeffs& c) : C(c) {}
+  __device__ int diff_kind() const { return C.diffusion_kind; }
+  __device__ bool has_adv() const { return C.has_advection; }
+  __device__ bool has_reac() const { return C.has_reaction; }
+  __device__ bool has_src() const { return C.has_source; }
+  __device__ bool has_dir() const { return C.has_dirichlet; }
+  __device__ bool has_neu() const { return C.has_neumann; }
+  __device__ double a_iso(const double* x) const { return eval_prog(C, C.diffusion[0], x); }
+  __device__ double a_ij(int i, int j, const double* x) const { return eval_prog(C, C.diffusion[i * DIM + j], x); }
+  __device__ double b_i(int i, const double* x) const { return eval_prog(C, C.advection[i], x); }
+  __device__ double c(const double* x) const { return eval_prog(C, C.reaction, x); }
+  __device__ double f(const double* x) const { return eval_prog(C, C.source, x); }
+  __device__ double gD(const double* x) const { return eval_prog(C, C.dirichlet, x); }
+  __device__ double gN(const double* x) const { return eval_prog(C, C.neumann, x); }
+};
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// 16-byte asynchronous global -> shared copies (LDGSTS), L2 only
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int DIM>
+__device__ __forceinline__ BoxConst<DIM> load_box(const double* erec, int64_t e) {
+  const double* r = erec + e * Widths<DIM>::ER;
+  BoxConst<DIM> b;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    b.c[i] = r[i];
+    b.ih[i] = r[DIM + i];
+    b.rs[i] = r[2 * DIM + i];
+  }
+  return b;
+}
+
+// x = v0 + xi E from a frame record (v0 then E rows), returns the stored measure
+template <int DIM, int K>
+__device__ __forceinline__ double frame_point(const double* fr, const double* xi, double* x) {
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    double acc = fr[i];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc += xi[j] * fr[DIM + j * DIM + i];
+    x[i] = acc;
+  }
+  return fr[DIM + K * DIM];
+}
+
+// Store one C tile set into rows of the element's row block (optionally
+// with its mirror image for symmetric accumulation).
+template <int NT, bool SYM>
+__device__ __forceinline__ void store_block(double* values, int64_t voff, int64_t L, int64_t col0, int ne,
+                                            int nj, const double (&c)[NT][NT][2], int g, int t) {
+#pragma unroll
+  for (int r = 0; r < NT; ++r) {
+#pragma unroll
+    for (int cc = 0; cc < NT; ++cc) {
+      if (SYM && cc < r) continue;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = r * 8 + g, j = cc * 8 + 2 * t + u;
+        if (i < ne && j < nj) values[voff + (int64_t)i * L + col0 + j] = c[r][cc][u];
+        if (SYM && cc > r && j < ne && i < nj) values[voff + (int64_t)j * L + col0 + i] = c[r][cc][u];
+      }
+    }
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void zero_tiles(double (&c)[NT][NT][2]) {
+#pragma unroll
+  for (int r = 0; r < NT; ++r)
+#pragma unroll
+    for (int cc = 0; cc < NT; ++cc) c[r][cc][0] = c[r][cc][1] = 0.0;
+}
+
+// Face trace values at one point: V_f and the flux F_f = n.(A grad phi_f)
+template <int DIM, int P, class CF>
+__device__ __forceinline__ double face_flux(const CF& cf, const Tab<DIM, P>& tb, int f, const double* nrm,
+                                            double a, const double (&A)[DIM][DIM]) {
+  double fl = 0.0;
+  if (cf.diff_kind() == PDG_DIFF_FULL) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      double ag = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < DIM; ++jj) ag += A[i][jj] * tb.grad(f, jj);
+      fl += nrm[i] * ag;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) fl += nrm[i] * tb.grad(f, i);
+    fl *= a;
+  }
+  return fl;
+}
+
+// KV: volume slots per round when known at compile time (runtime-specialised
+// kernels), 0 = read a.lay.kv.
+template <int DIM, int P, bool SYM, class CF, int KV = 0>
+__device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
+  using S = Shape<DIM, P>;
+  using W = Widths<DIM>;
+  constexpr int NB = S::NB, NT = S::NT, NBP = S::NBP;
+  extern __shared__ double smem[];
+  const pdg_mesh& m = a.m;
+  const pdg_basis& B = a.B;
+  const pdg_rules& R = a.R;
+  const pdg_pattern& pat = a.pat;
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double* buf = smem + (threadIdx.x >> 5) * a.lay.warp_doubles;
+  double* sc1 = buf + a.lay.buf_doubles;
+  double* sc2 = sc1 + 32;
+  // interface records of the current / next element's first neighbour window
+  pdg_iface_rec* recs = reinterpret_cast<pdg_iface_rec*>(sc2 + 32);  // [2][NBR_WIN]
+  double* rhs_s = reinterpret_cast<double*>(recs + 2 * NBR_WIN);    // [NB][32] when !RHS_REGS
+  // async-copied geometry: the element's simplex frames, the window's first facet frames
+  double* sfr = rhs_s + (S::RHS_REGS ? 0 : 32 * NB);
+  double* ffr = sfr + FR_MAX * W::SF;
+
+  const int kv = KV ? KV : a.lay.kv, kvp = kv + 4;
+  const int dk = cf.diff_kind();
+  const int nG = dk != PDG_DIFF_NONE ? DIM : 0;
+  const bool full = dk == PDG_DIFF_FULL;
+  const bool has_vr = cf.has_adv() || cf.has_reac();
+  const int rAG = nG, rV = nG + (full ? DIM : 0), rR = rV + 1;
+  const bool grad_terms = dk != PDG_DIFF_NONE && a.prm.include_gradient_terms;
+  // Isotropic diffusion: the volume table holds sqrt(w a) dphi, so the
+  // k-step feeds the same fragment as both DMMA operands (no per-k-step
+  // weighting, half the fragment loads).  Needs a(x) >= 0; a negative value
+  // raises PDG_FLAG_NEG_DIFFUSION and the host re-runs with PDG_OPT_PLAIN_VOLUME.
+  const bool sqrtw = dk == PDG_DIFF_ISO && !(a.prm.options & PDG_OPT_PLAIN_VOLUME);
+  const int mode = a.mode;
+
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // Asynchronous staging one element ahead (cp.async, issued while the
+  // current element's faces run): the simplex frames of element kk into sfr
+  // (if they fit) and the interface records of its first neighbour window
+  // into recs[rb].  The caller commits the group.
+  auto issue_next = [&](int64_t kk, int rb) -> bool {
+    if (kk >= pat.n_row_elements) return false;
+    const int32_t en = pat.row_elements ? pat.row_elements[kk] : (int32_t)kk;
+    if (!mode) {
+      const int64_t r0n = pat.nbr_ptr[en];
+      const int nwn = min(NBR_WIN, (int)(pat.nbr_ptr[en + 1] - r0n));
+      const double* rsrc = reinterpret_cast<const double*>(pat.nbr_rec + r0n);
+      double* rdst = reinterpret_cast<double*>(recs + rb * NBR_WIN);
+      for (int c = lane; c < nwn * 4; c += 32) cp_async16(rdst + 2 * c, rsrc + 2 * c);
+    }
+    const int64_t s0n = m.elem_ptr[en];
+    const int nsn = (int)(m.elem_ptr[en + 1] - s0n);
+    if (nsn > FR_MAX) return false;
+    const double* src = a.sframe + s0n * W::SF;
+    for (int c = lane; c < nsn * W::SF / 2; c += 32) cp_async16(sfr + 2 * c, src + 2 * c);
+    return true;
+  };
+  // first facet frame of every non-self interface of a staged window -> ffr[entry]
+  auto issue_ffr = [&](const pdg_iface_rec* rw, int nw, int32_t e) {
+    if (lane < nw && rw[lane].j != e) {
+      const double* src = a.fframe + (int64_t)rw[lane].row0 * W::FF;
+#pragma unroll
+      for (int c = 0; c < W::FF / 2; ++c) cp_async16(ffr + lane * W::FF + 2 * c, src + 2 * c);
+    }
+  };
+  int rb = 0;
+  bool next_frames = issue_next(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, rb);
+  cp_async_commit();
+  for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < pat.n_row_elements;
+       k += nwarps, rb ^= 1) {
+    const bool fr_smem = next_frames;
+    cp_async_wait_all();
+    __syncwarp();
+    const int32_t e = pat.row_elements ? pat.row_elements[k] : (int32_t)k;
+    pdg_iface_rec* rc = recs + rb * NBR_WIN;
+    const int64_t q0 = mode ? 0 : pat.nbr_ptr[e];
+    const int nnb = mode ? 0 : (int)(pat.nbr_ptr[e + 1] - q0);
+    // the first window's facet frames land during the volume phase
+    issue_ffr(rc, min(NBR_WIN, nnb), e);
+    cp_async_commit();
+    const int pe = B.degree[e];
+    const int64_t dof_e = B.dof_offset[e];
+    const int ne = (int)(B.dof_offset[e + 1] - dof_e);
+    const BoxConst<DIM> bx = load_box<DIM>(a.erec, e);
+    const int64_t voff = mode ? k * NB * NB : pat.elem_val_offset[k];
+    const int64_t Lrow = mode ? NB : pat.row_len[k];
+
+    double cd[NT][NT][2];
+    zero_tiles<NT>(cd);
+    double racc[S::RHS_REGS ? NB : 1];
+#pragma unroll
+    for (int f = 0; f < (S::RHS_REGS ? NB : 1); ++f) racc[f] = 0.0;
+    if (!S::RHS_REGS)
+      for (int f = 0; f < NB; ++f) rhs_s[f * 32 + lane] = 0.0;
+    auto rhs_add = [&](int f, double v) {
+      if constexpr (S::RHS_REGS) racc[f] += v;
+      else rhs_s[f * 32 + lane] += v;
+    };
+
+    // ------------------------------------------------------------ volume
+    {
+      const int order = 2 * pe + a.prm.quad_increment;
+      const int r0 = R.vol_offset[order], nq = R.vol_count[order];
+      const int64_t s0 = m.elem_ptr[e];
+      const int Q = (int)(m.elem_ptr[e + 1] - s0) * nq;
+      for (int base = 0; base < Q; base += kv) {
+        const int nvalid = min(kv, Q - base);
+        if (lane < kv) {
+          const int gq = base + min(lane, nvalid - 1);
+          const double valid = lane < nvalid ? 1.0 : 0.0;
+          const int ls = gq / nq;
+          const int kq = gq - ls * nq;
+          const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+          double x[3] = {0.0, 0.0, 0.0};
+          const double* fr = fr_smem ? sfr + ls * W::SF : a.sframe + (s0 + ls) * W::SF;
+          const double det = frame_point<DIM, DIM>(fr, xi, x);
+          const double w = R.weights[r0 + kq] * det * valid;
+          Tab<DIM, P> tb;
+          tb.load(bx, x);
+          double* col = buf + lane;
+          if (nG && sqrtw) {
+            const double av = cf.a_iso(x);
+            if (av < 0.0) raise_flag(a.flags, PDG_FLAG_NEG_DIFFUSION);
+            const double sw = R.sqrt_weights[r0 + kq] * fr[DIM + DIM * DIM + 1] * sqrt(fmax(av, 0.0)) * valid;
+            Tab<DIM, P> ts = tb;
+            ts.scale(sw);
+#pragma unroll
+            for (int c = 0; c < DIM; ++c)
+#pragma unroll
+              for (int f = 0; f < NBP; ++f) col[(c * NBP + f) * kvp] = f < NB ? ts.grad(f, c) : 0.0;
+          } else if (nG) {
+            const double av = dk == PDG_DIFF_ISO ? cf.a_iso(x) : 1.0;
+            sc1[lane] = w * av;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c)
+#pragma unroll
+              for (int f = 0; f < NBP; ++f) col[(c * NBP + f) * kvp] = f < NB ? tb.grad(f, c) : 0.0;
+            if (full) {
+              double A[DIM][DIM];
+#pragma unroll
+              for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                for (int j = 0; j < DIM; ++j) A[i][j] = cf.a_ij(i, j, x);
+#pragma unroll
+              for (int c = 0; c < DIM; ++c)
+#pragma unroll
+                for (int f = 0; f < NBP; ++f) {
+                  double v = 0.0;
+                  if (f < NB) {
+#pragma unroll
+                    for (int j = 0; j < DIM; ++j) v += A[c][j] * tb.grad(f, j);
+                  }
+                  col[((rAG + c) * NBP + f) * kvp] = v;
+                }
+            }
+          }
+          if (has_vr) {
+            sc2[lane] = w;
+            double bvec[DIM];
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) bvec[i] = cf.has_adv() ? cf.b_i(i, x) : 0.0;
+            const double cr = cf.has_reac() ? cf.c(x) : 0.0;
+#pragma unroll
+            for (int f = 0; f < NBP; ++f) {
+              double vv = 0.0, rr = 0.0;
+              if (f < NB) {
+                vv = tb.val(f);
+                if (cf.has_adv()) {
+#pragma unroll
+                  for (int i = 0; i < DIM; ++i) rr += bvec[i] * tb.grad(f, i);
+                }
+                if (cf.has_reac()) rr += cr * vv;
+              }
+              col[(rV * NBP + f) * kvp] = vv;
+              col[(rR * NBP + f) * kvp] = rr;
+            }
+          }
+          if (cf.has_src()) {
+            const double wf = w * cf.f(x);
+#pragma unroll
+            for (int f = 0; f < NB; ++f) rhs_add(f, wf * tb.val(f));
+          }
+        }
+        __syncwarp();
+        const int nk = (nvalid + 3) >> 2;
+        auto vol_kstep = [&](int kk) {
+          const int q = kk * 4 + t;
+          if (nG && sqrtw) {
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+              double fr_[NT];
+#pragma unroll
+              for (int i = 0; i < NT; ++i) fr_[i] = buf[(c * NBP + i * 8 + g) * kvp + q];
+#pragma unroll
+              for (int r = 0; r < NT; ++r)
+#pragma unroll
+                for (int cc = 0; cc < NT; ++cc)
+                  if (!SYM || cc >= r) dmma(cd[r][cc], fr_[r], fr_[cc]);
+            }
+          } else if (nG) {
+            const double s1 = sc1[q];
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+              double lf[NT], rf[NT];
+#pragma unroll
+              for (int i = 0; i < NT; ++i) {
+                const double gv = buf[(c * NBP + i * 8 + g) * kvp + q];
+                lf[i] = s1 * gv;
+                rf[i] = full ? buf[((rAG + c) * NBP + i * 8 + g) * kvp + q] : gv;
+              }
+#pragma unroll
+              for (int r = 0; r < NT; ++r)
+#pragma unroll
+                for (int cc = 0; cc < NT; ++cc)
+                  if (!SYM || cc >= r) dmma(cd[r][cc], lf[r], rf[cc]);
+            }
+          }
+          if (has_vr) {
+            const double s2 = sc2[q];
+            double lf[NT], rf[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+              lf[i] = s2 * buf[(rV * NBP + i * 8 + g) * kvp + q];
+              rf[i] = buf[(rR * NBP + i * 8 + g) * kvp + q];
+            }
+#pragma unroll
+            for (int r = 0; r < NT; ++r)
+#pragma unroll
+              for (int cc = 0; cc < NT; ++cc)
+                if (!SYM || cc >= r) dmma(cd[r][cc], lf[r], rf[cc]);
+          }
+        };
+        if (KV && nk == KV / 4) {
+          // full chunk of a runtime-specialised kernel: fixed trip count and
+          // compile-time table offsets
+#pragma unroll
+          for (int kk = 0; kk < KV / 4; ++kk) vol_kstep(kk);
+        } else {
+          PDG_UNROLL(PDG_VOL_UNROLL)
+          for (int kk = 0; kk < nk; ++kk) vol_kstep(kk);
+        }
+        __syncwarp();
+      }
+    }
+
+    // the volume phase is done with sfr: start copying the next element's
+    // simplex frames and records while this element's faces are processed
+    __syncwarp();
+    next_frames = issue_next(k + nwarps, rb ^ 1);
+    cp_async_commit();
+
+    // ------------------------------------------------------------ interfaces
+    // Neighbour entries are staged NBR_WIN at a time as interface records
+    // (pdg_iface_rec: element, DoF count, column start, face range and the
+    // first face's metadata, flattened by pdg_iface_records; the first window
+    // arrives by cp.async during the previous element's faces), so the face
+    // loop reads shared memory instead of chains of dependent global loads.  Two interfaces made of a single sub-facet with <= 8
+    // quadrature points (every 2D Voronoi interface up to p = 6) share one
+    // tabulation round: slots 0-7 / 8-15, own trace on lanes 0-15, the
+    // neighbour's on lanes 16-31.
+    int64_t colself = 0;
+    const bool mine = lane < KF;
+    const int slot = lane & (KF - 1);
+
+    // tabulate one face slot: own trace (lanes 0-15) or neighbour trace (16-31)
+    auto tab_slot = [&](const double* nrm, const double* frp, int r0, int kq, double valid, double sig, double sgn,
+                        bool down, const BoxConst<DIM>& bo) {
+      const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+      double x[3] = {0.0, 0.0, 0.0};
+      const double jac = frame_point<DIM, DIM - 1>(frp, xi, x);
+      const double w = R.weights[r0 + kq] * jac * valid;
+      Tab<DIM, P> tb;
+      tb.load(mine ? bx : bo, x);
+      double av = 1.0;
+      double A[DIM][DIM];
+      if (grad_terms) {
+        if (full) {
+#pragma unroll
+          for (int i = 0; i < DIM; ++i)
+#pragma unroll
+            for (int jj = 0; jj < DIM; ++jj) A[i][jj] = cf.a_ij(i, jj, x);
+        } else {
+          av = cf.a_iso(x);
+        }
+      }
+      double* col = buf + slot;
+      const int rv = mine ? 0 : 2;
+      const double vs = mine ? 1.0 : -1.0;
+#pragma unroll
+      for (int ff = 0; ff < NBP; ++ff) {
+        double vv = 0.0, fl = 0.0;
+        if (ff < NB) {
+          vv = tb.val(ff);
+          if (grad_terms) fl = face_flux<DIM, P>(cf, tb, ff, nrm, av, A);
+        }
+        col[(rv * NBP + ff) * KFP] = vs * vv;
+        col[((rv + 1) * NBP + ff) * KFP] = fl;
+      }
+      if (mine) {
+        double wbn = 0.0;
+        if (down) {
+          double bn = 0.0;
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) bn += cf.b_i(i, x) * nrm[i];
+          wbn = w * bn;
+        }
+        sc1[slot] = w * sig - sgn * wbn;
+        sc2[slot] = grad_terms ? -0.5 * sgn * w : 0.0;
+      }
+    };
+    // contract k-steps [k0, k1) of the face table into the diagonal tiles and co
+    auto face_contract = [&](int k0, int k1, double (&co)[NT][NT][2]) {
+      PDG_UNROLL(PDG_FACE_UNROLL)
+      for (int kk = k0; kk < k1; ++kk) {
+        const int qq = kk * 4 + t;
+        const double al = sc1[qq], be = sc2[qq];
+        double va[NT], fa[NT], nvb[NT], fb[NT], l1[NT], l2[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          va[i] = buf[(0 * NBP + i * 8 + g) * KFP + qq];
+          nvb[i] = buf[(2 * NBP + i * 8 + g) * KFP + qq];
+          if (grad_terms) {
+            fa[i] = buf[(1 * NBP + i * 8 + g) * KFP + qq];
+            fb[i] = buf[(3 * NBP + i * 8 + g) * KFP + qq];
+            l1[i] = al * va[i] + be * fa[i];
+            l2[i] = be * va[i];
+          } else {
+            fa[i] = fb[i] = l2[i] = 0.0;
+            l1[i] = al * va[i];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < NT; ++r)
+#pragma unroll
+          for (int cc = 0; cc < NT; ++cc) {
+            if (!SYM || cc >= r) {
+              dmma(cd[r][cc], l1[r], va[cc]);
+              if (grad_terms) dmma(cd[r][cc], l2[r], fa[cc]);
+            }
+            dmma(co[r][cc], l1[r], nvb[cc]);
+            if (grad_terms) dmma(co[r][cc], l2[r], fb[cc]);
+          }
+      }
+    };
+
+    for (int w0 = 0; w0 < nnb; w0 += NBR_WIN) {
+      const int nw = min(NBR_WIN, nnb - w0);
+      if (w0 == 0) {
+        // this element's facet frames; the next element's copies stay in flight
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        // windows beyond the first (more than NBR_WIN neighbours): synchronous restage
+        __syncwarp();
+        const double* rsrc = reinterpret_cast<const double*>(pat.nbr_rec + q0 + w0);
+        for (int c = lane; c < nw * 4; c += 32) cp_async16(reinterpret_cast<double*>(rc) + 2 * c, rsrc + 2 * c);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        issue_ffr(rc, nw, e);
+        cp_async_commit();
+        cp_async_wait_all();
+      }
+      __syncwarp();
+      {
+        const unsigned selfm = __ballot_sync(0xffffffffu, lane < nw && rc[lane].j == e);
+        if (selfm) colself = rc[__ffs(selfm) - 1].col;
+      }
+      // col_idx of this window's column span, all rows (division-free)
+      if (a.write_cols) {
+        const int c0 = rc[0].col;
+        const int c1 = rc[nw - 1].col + rc[nw - 1].nj;
+        int q = 0;
+        for (int p = c0 + lane; p < c1; p += 32) {
+          while (q + 1 < nw && rc[q + 1].col <= p) ++q;
+          const int64_t cv = B.dof_offset[rc[q].j] + (p - rc[q].col);
+          int64_t* dst = pat.col_idx + voff + p;
+          for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
+        }
+      }
+      int qi = 0;
+      while (qi < nw) {
+        if (rc[qi].j == e) {
+          ++qi;
+          continue;
+        }
+        int qb = qi + 1;
+        if (qb < nw && rc[qb].j == e) ++qb;
+        const bool pair = (rc[qi].info & 4) && qb < nw && (rc[qb].info & 4);
+        double co[NT][NT][2];
+        zero_tiles<NT>(co);
+        if (pair) {
+          // ---- two single-facet interfaces in one round
+          const int seg = slot >> 3, ls = slot & 7;
+          const int q = seg ? qb : qi;
+          const int info = rc[q].info;
+          const int pj = rc[q].pj;
+          const int order = 2 * max(pe, pj) + a.prm.quad_increment;
+          const int r0 = R.face_offset[order], nq = R.face_count[order];
+          double nrm[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) nrm[i] = rc[q].nrm[i];
+          const BoxConst<DIM> bo = load_box<DIM>(a.erec, rc[q].j);
+          tab_slot(nrm, ffr + q * W::FF, r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, rc[q].sig,
+                   (info & 1) ? -1.0 : 1.0, (info & 2) != 0, bo);
+          __syncwarp();
+          face_contract(0, 2, co);
+          store_block<NT, false>(a.values, voff, Lrow, rc[qi].col, ne, rc[qi].nj, co, g, t);
+          zero_tiles<NT>(co);
+          face_contract(2, 4, co);
+          store_block<NT, false>(a.values, voff, Lrow, rc[qb].col, ne, rc[qb].nj, co, g, t);
+          __syncwarp();
+          qi = qb + 1;
+          continue;
+        }
+        // ---- general interface: every face, every sub-facet, rounds of 16 points
+        const int32_t j = rc[qi].j;
+        const int pj = rc[qi].pj;
+        const BoxConst<DIM> bo = load_box<DIM>(a.erec, j);
+        const int order = 2 * max(pe, pj) + a.prm.quad_increment;
+        const int r0 = R.face_offset[order], nq = R.face_count[order];
+        const int fend = rc[qi].fb;
+        for (int f = rc[qi].fa; f < fend; ++f) {
+          int side, info;
+          double sig;
+          double nrm[3] = {0.0, 0.0, 0.0};
+          int64_t row0;
+          int nrows;
+          if (f == rc[qi].fa) {
+            info = rc[qi].info;
+            side = info & 1;
+            sig = rc[qi].sig;
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) nrm[i] = rc[qi].nrm[i];
+            row0 = rc[qi].row0;
+          } else {
+            side = m.face_owner[f] == e ? 0 : 1;
+            info = side | ((cf.has_adv() && a.flow[f] == side) ? 2 : 0);
+            sig = a.sigma[f];
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)f * DIM + i];
+            row0 = m.face_ptr[f];
+          }
+          nrows = (int)(m.face_ptr[f + 1] - row0);
+          const int Pf = nrows * nq;
+          for (int base = 0; base < Pf; base += KF) {
+            const int nvalid = min(KF, Pf - base);
+            const int gq = base + min(slot, nvalid - 1);
+            const int lr = gq / nq;
+            tab_slot(nrm, a.fframe + (row0 + lr) * W::FF, r0, gq - lr * nq, slot < nvalid ? 1.0 : 0.0, sig,
+                     side ? -1.0 : 1.0, (info & 2) != 0, bo);
+            __syncwarp();
+            face_contract(0, (nvalid + 3) >> 2, co);
+            __syncwarp();
+          }
+        }
+        store_block<NT, false>(a.values, voff, Lrow, rc[qi].col, ne, rc[qi].nj, co, g, t);
+        ++qi;
+      }
+      __syncwarp();
+    }
+
+    // ------------------------------------------------------------ boundary faces
+    const int64_t bend = mode ? 0 : m.elem_bface_ptr[e + 1];
+    for (int64_t bi = mode ? 0 : m.elem_bface_ptr[e]; bi < bend; ++bi) {
+      const int32_t f = m.elem_bfaces[bi];
+      const int tag = m.face_tag[f];
+      if (tag == PDG_TAG_OUTFLOW || tag == PDG_TAG_INTERIOR) continue;
+      if (tag == PDG_TAG_NEUMANN && !cf.has_neu()) continue;
+      const bool matrix = tag != PDG_TAG_NEUMANN;
+      const double sig = a.sigma[f];
+      const bool wi = tag == PDG_TAG_DIRICHLET && cf.has_adv() && a.flow[f] == 1;
+      const int order = 2 * pe + a.prm.quad_increment;
+      const int r0 = R.face_offset[order], nq = R.face_count[order];
+      double nrm[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)f * DIM + i];
+      const int64_t row0 = m.face_ptr[f];
+      const int Pf = (int)(m.face_ptr[f + 1] - row0) * nq;
+      const int slot = lane & (KF - 1);
+      const bool mine = lane < KF;
+      const bool use_f = tag == PDG_TAG_DIRICHLET && grad_terms;
+      for (int base = 0; base < Pf; base += KF) {
+        const int nvalid = min(KF, Pf - base);
+        {
+          const int gq = base + min(slot, nvalid - 1);
+          const double valid = (slot < nvalid && mine) ? 1.0 : 0.0;
+          const int lr = gq / nq;
+          const int kq = gq - lr * nq;
+          const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+          double x[3] = {0.0, 0.0, 0.0};
+          const double jac = frame_point<DIM, DIM - 1>(a.fframe + (row0 + lr) * W::FF, xi, x);
+          const double w = R.weights[r0 + kq] * jac * valid;
+          Tab<DIM, P> tb;
+          tb.load(bx, x);
+          double av = 1.0;
+          double A[DIM][DIM];
+          if (use_f) {
+            if (full) {
+#pragma unroll
+              for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                for (int jj = 0; jj < DIM; ++jj) A[i][jj] = cf.a_ij(i, jj, x);
+            } else {
+              av = cf.a_iso(x);
+            }
+          }
+          double wbn = 0.0;
+          if ((wi || tag == PDG_TAG_INFLOW) && cf.has_adv()) {
+            double bn = 0.0;
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) bn += cf.b_i(i, x) * nrm[i];
+            wbn = w * bn;
+          }
+          double al = 0.0, be = 0.0, gval = 0.0;
+          if (tag == PDG_TAG_DIRICHLET) {
+            al = w * sig - (wi ? wbn : 0.0);
+            be = use_f ? -w : 0.0;
+            gval = cf.has_dir() ? cf.gD(x) : 0.0;
+          } else if (tag == PDG_TAG_INFLOW) {
+            al = -wbn;
+            gval = cf.has_dir() ? cf.gD(x) : 0.0;
+          } else {  // Neumann: load only
+            gval = w * cf.gN(x);
+          }
+          double* col = buf + slot;
+#pragma unroll
+          for (int ff = 0; ff < NBP; ++ff) {
+            double vv = 0.0, fl = 0.0;
+            if (ff < NB) {
+              vv = tb.val(ff);
+              if (use_f) fl = face_flux<DIM, P>(cf, tb, ff, nrm, av, A);
+              if (mine) {
+                if (tag == PDG_TAG_NEUMANN) rhs_add(ff, gval * vv);
+                else if (cf.has_dir()) rhs_add(ff, gval * (al * vv + be * fl));
+              }
+            }
+            if (mine && matrix) {
+              col[(0 * NBP + ff) * KFP] = vv;
+              col[(1 * NBP + ff) * KFP] = fl;
+            }
+          }
+          if (mine && matrix) {
+            sc1[slot] = al;
+            sc2[slot] = be;
+          }
+        }
+        __syncwarp();
+        if (matrix) {
+          const int nk = (nvalid + 3) >> 2;
+          for (int kk = 0; kk < nk; ++kk) {
+            const int qq = kk * 4 + t;
+            const double al = sc1[qq], be = sc2[qq];
+            double va[NT], fa[NT], l1[NT], l2[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+              va[i] = buf[(0 * NBP + i * 8 + g) * KFP + qq];
+              fa[i] = buf[(1 * NBP + i * 8 + g) * KFP + qq];
+              l1[i] = al * va[i] + be * fa[i];
+              l2[i] = be * va[i];
+            }
+#pragma unroll
+            for (int r = 0; r < NT; ++r)
+#pragma unroll
+              for (int cc = 0; cc < NT; ++cc)
+                if (!SYM || cc >= r) {
+                  dmma(cd[r][cc], l1[r], va[cc]);
+                  if (use_f) dmma(cd[r][cc], l2[r], fa[cc]);
+                }
+          }
+        }
+        __syncwarp();
+      }
+    }
+
+    // ------------------------------------------------------------ write-out
+    store_block<NT, SYM>(a.values, voff, Lrow, colself, ne, ne, cd, g, t);
+    double* rhs_out = mode ? a.rhs + k * NB : a.rhs + dof_e;
+    __syncwarp();
+    if constexpr (S::RHS_REGS) {
+#pragma unroll
+      for (int f = 0; f < NB; ++f) buf[lane * NB + f] = racc[f];
+      __syncwarp();
+      for (int f = lane; f < ne; f += 32) {
+        double s = 0.0;
+        for (int l = 0; l < 32; ++l) s += buf[l * NB + f];
+        rhs_out[f] = s;
+      }
+    } else {
+      __syncwarp();
+      for (int f = lane; f < ne; f += 32) {
+        double s = 0.0;
+        for (int l = 0; l < 32; ++l) s += rhs_s[f * 32 + l];
+        rhs_out[f] = s;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace pdg

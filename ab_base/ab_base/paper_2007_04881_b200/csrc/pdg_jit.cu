@@ -1,0 +1,323 @@
+// Runtime specialisation of the element kernel (NVRTC -> sm_100a cubin).
+//
+// The coefficient fields of one problem are known only at run time (they
+// are Python expressions).  The ahead-of-time kernels interpret them from
+// bytecode, which costs a dispatch loop + a local-memory stack per field per
+// quadrature point and keeps every "has advection / full tensor ..." test a
+// runtime branch.  Here the generated policy class (model.py
+// ``policy_source``) is compiled together with assemble_body.cuh, so fields
+// are inlined expressions and the kind flags are compile-time constants: the
+// compiler drops the unused paths, registers and instruction-cache pressure
+// fall, and sin(pi*x) etc. are scheduled with the tabulation.
+//
+// libnvrtc and libcuda are opened with dlopen on first use, so the library
+// itself links only against cudart (it must load on GPU-less build hosts).
+// Compiled cubins are cached in memory and on disk ($PDG_JIT_CACHE, default
+// <libdir>/jit_cache) keyed by the full source + options.
+#include <dlfcn.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <unordered_map>
+#include <vector>
+
+#include "assemble_kernel.cuh"
+#include "assemble_ws.cuh"
+
+namespace pdg {
+
+// ---- minimal driver / NVRTC API surface (resolved with dlsym) ---------------
+typedef int CUres;
+typedef struct CUmod_st* CUmod;
+typedef struct CUfunc_st* CUfunc;
+typedef int nvrtcRes;
+typedef struct _nvrtcProgram* nvrtcProg;
+
+struct Api {
+  bool ok = false;
+  std::string why;
+  CUres (*cuModuleLoadData)(CUmod*, const void*);
+  CUres (*cuModuleGetFunction)(CUfunc*, CUmod, const char*);
+  CUres (*cuFuncSetAttribute)(CUfunc, int, int);
+  CUres (*cuLaunchKernel)(CUfunc, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                          cudaStream_t, void**, void**);
+  CUres (*cuOccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunc, int, size_t);
+  nvrtcRes (*nvrtcCreateProgram)(nvrtcProg*, const char*, const char*, int, const char* const*,
+                                 const char* const*);
+  nvrtcRes (*nvrtcCompileProgram)(nvrtcProg, int, const char* const*);
+  nvrtcRes (*nvrtcGetProgramLogSize)(nvrtcProg, size_t*);
+  nvrtcRes (*nvrtcGetProgramLog)(nvrtcProg, char*);
+  nvrtcRes (*nvrtcGetCUBINSize)(nvrtcProg, size_t*);
+  nvrtcRes (*nvrtcGetCUBIN)(nvrtcProg, char*);
+  nvrtcRes (*nvrtcDestroyProgram)(nvrtcProg*);
+};
+
+constexpr int CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES_ = 8;
+
+static Api& api() {
+  static Api a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* cu = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    void* rtc = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!rtc) rtc = dlopen("libnvrtc.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!cu || !rtc) {
+      a.why = std::string("cannot dlopen ") + (!cu ? "libcuda.so.1 " : "") + (!rtc ? "libnvrtc.so.12" : "");
+      return;
+    }
+#define PDG_SYM(lib, name)                                               \
+  a.name = reinterpret_cast<decltype(a.name)>(dlsym(lib, #name));        \
+  if (!a.name) {                                                         \
+    a.why = "missing symbol " #name;                                     \
+    return;                                                              \
+  }
+    PDG_SYM(cu, cuModuleLoadData)
+    PDG_SYM(cu, cuModuleGetFunction)
+    PDG_SYM(cu, cuFuncSetAttribute)
+    PDG_SYM(cu, cuLaunchKernel)
+    PDG_SYM(cu, cuOccupancyMaxActiveBlocksPerMultiprocessor)
+    PDG_SYM(rtc, nvrtcCreateProgram)
+    PDG_SYM(rtc, nvrtcCompileProgram)
+    PDG_SYM(rtc, nvrtcGetProgramLogSize)
+    PDG_SYM(rtc, nvrtcGetProgramLog)
+    PDG_SYM(rtc, nvrtcGetCUBINSize)
+    PDG_SYM(rtc, nvrtcGetCUBIN)
+    PDG_SYM(rtc, nvrtcDestroyProgram)
+#undef PDG_SYM
+    a.ok = true;
+  });
+  return a;
+}
+
+static std::string lib_dir() {
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void*>(&pdg_abi_version), &info) && info.dli_fname) {
+    std::string p(info.dli_fname);
+    const size_t k = p.rfind('/');
+    return k == std::string::npos ? std::string(".") : p.substr(0, k);
+  }
+  return ".";
+}
+
+static uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+struct JitKernel {
+  CUmod mod = nullptr;
+  CUfunc fn = nullptr;
+};
+
+static std::mutex g_mu;
+static std::unordered_map<std::string, JitKernel> g_cache;
+
+// PDG_RHS_REGS_MAX for runtime compiles (env override for experiments)
+static int jit_rhs_regs_max() {
+  const char* v = getenv("PDG_RHS_REGS_MAX");
+  return v ? atoi(v) : PDG_RHS_REGS_MAX;
+}
+
+// PDG_WS=1 selects the warp-specialised producer/consumer body
+// (assemble_ws.cuh) instead of the single-warp body (assemble_body.cuh).
+// Measured on 400k cfg5 cells (r1): single-warp 7.51 ms, WS 10.0 ms -- the
+// producer (tabulation + metadata) is the bottleneck, so WS is off by default.
+static bool jit_ws() {
+  const char* v = getenv("PDG_WS");
+  return v && v[0] == '1';
+}
+
+static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv) {
+  // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow.
+  // single-warp body: CTA = 128 threads, default 3 (168 registers, 12 warps/SM;
+  //   v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells);
+  // warp-specialised body: CTA = 64 threads (one pair), default 8 (128 registers)
+  const bool ws = jit_ws();
+  const char* mb = getenv("PDG_JIT_MINBLOCKS");
+  const int minblocks = mb ? std::max(1, atoi(mb)) : (ws ? 8 : 3);
+  std::ostringstream os;
+  os << "#include \"" << (ws ? "assemble_ws.cuh" : "assemble_body.cuh") << "\"\n"
+     << "namespace pdg_jit {\nusing namespace pdg;\n"
+     << policy << "\n}\n"
+     << "extern \"C\" __global__ void __launch_bounds__(" << (ws ? 64 : 128) << ", " << minblocks
+     << ") pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {\n"
+     << "  pdg::" << (ws ? "assemble_ws<" : "assemble_body<") << dim << ", " << P << ", "
+     << (sym ? "true" : "false");
+  if (!ws) os << ", pdg_jit::JitCoef, " << kv;
+  os << ">(a, pdg_jit::JitCoef());\n}\n";
+  return os.str();
+}
+
+static bool read_file(const std::string& path, std::string& out) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  std::ostringstream ss;
+  ss << f.rdbuf();
+  out = ss.str();
+  return true;
+}
+
+// compile or fetch; returns empty string on success, else the error
+static std::string get_kernel(const std::string& policy, int dim, int P, bool sym, int kv, JitKernel& out) {
+  Api& A = api();
+  if (!A.ok) return "JIT unavailable: " + A.why;
+  const std::string dir = lib_dir();
+  const std::string src = full_source(policy, dim, P, sym, kv);
+  std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                                   "-DPDG_RHS_REGS_MAX=" + std::to_string(jit_rhs_regs_max()),
+                                   "-I" + dir + "/csrc",
+                                   "-I" + dir + "/../include"};
+  // PDG_JIT_DEFINES: extra space-separated -D options (tuning experiments)
+  if (const char* defs = getenv("PDG_JIT_DEFINES")) {
+    std::istringstream is(defs);
+    std::string tok;
+    while (is >> tok) opts.push_back(tok);
+  }
+  std::string key = src;
+  for (auto& o : opts) key += "\n" + o;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {
+      out = it->second;
+      return "";
+    }
+  }
+  // disk cache: file = 16 hex digits of the key hash; content = key size, key, cubin
+  const char* env = getenv("PDG_JIT_CACHE");
+  const std::string cdir = env ? std::string(env) : dir + "/jit_cache";
+  char hex[32];
+  snprintf(hex, sizeof(hex), "%016llx", (unsigned long long)fnv1a(key));
+  const std::string cpath = cdir + "/" + hex + ".cubin";
+  std::string cubin, blob;
+  if (read_file(cpath, blob) && blob.size() > 8) {
+    uint64_t klen = 0;
+    std::memcpy(&klen, blob.data(), 8);
+    if (klen + 8 <= blob.size() && blob.compare(8, klen, key) == 0) cubin = blob.substr(8 + klen);
+  }
+  if (cubin.empty()) {
+    nvrtcProg prog;
+    if (A.nvrtcCreateProgram(&prog, src.c_str(), "pdg_jit.cu", 0, nullptr, nullptr) != 0)
+      return "nvrtcCreateProgram failed";
+    std::vector<const char*> co;
+    for (auto& o : opts) co.push_back(o.c_str());
+    const nvrtcRes rc = A.nvrtcCompileProgram(prog, (int)co.size(), co.data());
+    size_t lsz = 0;
+    A.nvrtcGetProgramLogSize(prog, &lsz);
+    std::string log(lsz, '\0');
+    if (lsz) A.nvrtcGetProgramLog(prog, &log[0]);
+    if (rc != 0) {
+      A.nvrtcDestroyProgram(&prog);
+      return "NVRTC compile failed:\n" + log;
+    }
+    size_t csz = 0;
+    A.nvrtcGetCUBINSize(prog, &csz);
+    cubin.resize(csz);
+    A.nvrtcGetCUBIN(prog, &cubin[0]);
+    A.nvrtcDestroyProgram(&prog);
+    // best-effort disk cache (atomic rename)
+    std::string cmd = "mkdir -p '" + cdir + "' 2>/dev/null";
+    if (system(cmd.c_str()) == 0) {
+      const std::string tmp = cpath + ".tmp" + std::to_string((long long)getpid());
+      std::ofstream f(tmp, std::ios::binary);
+      if (f) {
+        const uint64_t klen = key.size();
+        f.write(reinterpret_cast<const char*>(&klen), 8);
+        f.write(key.data(), (std::streamsize)key.size());
+        f.write(cubin.data(), (std::streamsize)cubin.size());
+        f.close();
+        rename(tmp.c_str(), cpath.c_str());
+      }
+    }
+  }
+  cudaFree(nullptr);  // make sure the runtime's primary context is current
+  JitKernel k;
+  if (A.cuModuleLoadData(&k.mod, cubin.data()) != 0) return "cuModuleLoadData failed";
+  if (A.cuModuleGetFunction(&k.fn, k.mod, "pdg_jit_kernel") != 0) return "cuModuleGetFunction failed";
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_cache[key] = k;
+  }
+  out = k;
+  return "";
+}
+
+KArgs make_kargs(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_rules* rules, const pdg_params* params,
+                 const pdg_pattern& pat, const pdg_frames* frames, const double* sigma, const int8_t* flow,
+                 double* values, int write_cols, double* rhs, uint32_t* flags, int mode);
+
+}  // namespace pdg
+
+using namespace pdg;
+
+extern "C" int pdg_jit_prepare(const pdg_coeffs* coeffs, const char* policy_source, int32_t dim,
+                               int32_t max_degree) {
+  PDG_TRY {
+    if (!coeffs || !policy_source) return fail(PDG_ERR_INVALID, "null argument");
+    JitKernel k;
+    const int kv = make_layout(dim, max_degree, coeffs->diffusion_kind,
+                               coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max()).kv;
+    const std::string err = get_kernel(policy_source, dim, max_degree, symmetric_accumulation(*coeffs), kv, k);
+    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                                const char* policy_source, const pdg_rules* rules, const pdg_params* params,
+                                const pdg_pattern* pattern, const pdg_frames* frames, const double* sigma,
+                                const int8_t* face_flow, double* values, int32_t write_col_idx, double* rhs,
+                                uint32_t* err_flags, pdg_stream stream) {
+  PDG_TRY {
+    int rc = check_common(mesh, basis, coeffs);
+    if (rc) return rc;
+    if (!policy_source || !rules || !rules->sqrt_weights || !params || !pattern || !frames || !sigma || !face_flow || !values || !rhs)
+      return fail(PDG_ERR_INVALID, "null argument");
+    if (write_col_idx && !pattern->col_idx) return fail(PDG_ERR_INVALID, "col_idx not allocated");
+    if (!pattern->nbr_rec) return fail(PDG_ERR_INVALID, "interface records missing (pdg_iface_records)");
+    JitKernel k;
+    const bool sym = symmetric_accumulation(*coeffs);
+    const bool ws = jit_ws();
+    const bool has_vr = coeffs->has_advection || coeffs->has_reaction;
+    KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values, write_col_idx,
+                         rhs, err_flags, 0);
+    a.lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, jit_rhs_regs_max());
+    const std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, sym, a.lay.kv, k);
+    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
+    int threads = 128;
+    size_t smem = (size_t)a.lay.warp_doubles * 8 * (threads / 32);
+    if (ws) {  // one producer/consumer pair per CTA: two stages + header + neighbour staging
+      int kv = 32;
+      a.lay.buf_doubles = ws_table_doubles(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, &kv);
+      a.lay.kv = kv;
+      threads = 64;
+      smem = (size_t)2 * (a.lay.buf_doubles + 64 + sizeof(WsHdr) / 8) * 8 + sizeof(NbrStage);
+    }
+    Api& A = api();
+    if (A.cuFuncSetAttribute(k.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES_, (int)smem) != 0)
+      return fail(PDG_ERR_CUDA, "cuFuncSetAttribute(max dynamic smem) failed");
+    int per_sm = 0;
+    if (A.cuOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, threads, smem) != 0 || per_sm < 1) per_sm = 1;
+    const int64_t need = ws ? pattern->n_row_elements : (pattern->n_row_elements + 3) / 4;
+    const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm * (ws ? 1 : 8));
+    if (grid <= 0) return PDG_OK;
+    void* args[] = {&a};
+    if (A.cuLaunchKernel(k.fn, (unsigned)grid, 1, 1, threads, 1, 1, (unsigned)smem, (cudaStream_t)stream, args,
+                         nullptr) != 0)
+      return fail(PDG_ERR_CUDA, "cuLaunchKernel failed");
+    note_launch();
+    return PDG_OK;
+  }
+  PDG_CATCH
+}

@@ -1,0 +1,386 @@
+// Face pre-pass: penalty parameter and flow side of every face.
+//
+//  sigma_F = C * max_{k in sides} min(|k| / sup|K^F|, cov_cap) * a_bar_k * p_k^2 * |F| / |k|
+//      (polydg model.py:238-257, side data model.py:196-235, MeshGeometry.face_sigma
+//       assembly.py:613-626), a_bar_k = max over k's volume quadrature points of
+//       n^T A(x) n with the face (owner) normal;
+//  flow side: sign of the mean of b.n over the order-2 sample points of the
+//      face's sub-facets, straddle check (model.py:118-135,176-191), upwind
+//      attribution (assembly.py:596-611).
+//
+// sigma needs the a_bar of BOTH sides before any face term can be formed, so
+// it runs as a separate, cheap launch ahead of the element kernel.
+#include "pdg_internal.cuh"
+
+namespace pdg {
+
+template <int DIM>
+__device__ __forceinline__ double nAn(const pdg_coeffs& C, const double* n, const double* x) {
+  if (C.diffusion_kind == PDG_DIFF_ISO) {
+    const double a = eval_prog(C, C.diffusion[0], x);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) s += n[i] * a * n[i];
+    return s;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) r += eval_prog(C, C.diffusion[i * DIM + j], x) * n[j];
+    s += n[i] * r;
+  }
+  return s;
+}
+
+__device__ __forceinline__ bool diffusion_is_constant(const pdg_coeffs& C, int dim) {
+  if (C.diffusion_kind == PDG_DIFF_ISO) return C.diffusion[0].is_const;
+  for (int k = 0; k < dim * dim; ++k)
+    if (!C.diffusion[k].is_const) return false;
+  return true;
+}
+
+// max over an element's volume quadrature points of a(x) (isotropic a(x) I):
+// one warp per element, lanes over points, warp max.
+template <int DIM>
+__global__ void elem_abar_iso(const pdg_mesh m, const pdg_basis B, const __grid_constant__ pdg_coeffs C,
+                              const pdg_rules R, const pdg_params prm, double* abar, uint32_t* flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < m.n_elements; e += nwarps) {
+    const int order = 2 * B.degree[e] + prm.quad_increment;
+    const int r0 = R.vol_offset[order], nq = R.vol_count[order];
+    const int64_t s0 = m.elem_ptr[e];
+    const int64_t Q = (m.elem_ptr[e + 1] - s0) * nq;
+    double best = -INFINITY;
+    for (int64_t g = lane; g < Q; g += 32) {
+      const int s = m.elem_simplices[s0 + g / nq];
+      const int k = (int)(g % nq);
+      double v0[3], E[3][3];
+      simplex_frame<DIM>(m, s, v0, E, flags);
+      double x[3] = {0, 0, 0};
+      const double* xi = R.points + (int64_t)(r0 + k) * 3;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        double acc = v0[i];
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) acc += xi[j] * E[j][i];
+        x[i] = acc;
+      }
+      best = fmax(best, eval_prog(C, C.diffusion[0], x));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) abar[e] = best;
+  }
+}
+
+template <int DIM>
+__device__ double side_abar(const pdg_mesh& m, const pdg_basis& B, const pdg_coeffs& C,
+                            const pdg_rules& R, const pdg_params& prm, const double* abar_iso,
+                            int32_t el, const double* n, uint32_t* flags) {
+  if (C.diffusion_kind == PDG_DIFF_NONE) return 0.0;
+  double x0[3] = {0, 0, 0};
+  if (diffusion_is_constant(C, DIM)) return nAn<DIM>(C, n, x0);
+  if (C.diffusion_kind == PDG_DIFF_ISO) {
+    double nn = 0.0;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) nn += n[i] * n[i];
+    return abar_iso[el] * nn;
+  }
+  // general variable tensor: loop over the element's volume points
+  const int order = 2 * B.degree[el] + prm.quad_increment;
+  const int r0 = R.vol_offset[order], nq = R.vol_count[order];
+  double best = -INFINITY;
+  for (int64_t si = m.elem_ptr[el]; si < m.elem_ptr[el + 1]; ++si) {
+    double v0[3], E[3][3];
+    simplex_frame<DIM>(m, m.elem_simplices[si], v0, E, flags);
+    for (int k = 0; k < nq; ++k) {
+      const double* xi = R.points + (int64_t)(r0 + k) * 3;
+      double x[3] = {0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        double acc = v0[i];
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) acc += xi[j] * E[j][i];
+        x[i] = acc;
+      }
+      best = fmax(best, nAn<DIM>(C, n, x));
+    }
+  }
+  return best;
+}
+
+template <int DIM>
+__global__ void face_prepass(const pdg_mesh m, const pdg_basis B, const __grid_constant__ pdg_coeffs C,
+                             const pdg_rules R, const pdg_params prm, const double* abar_iso,
+                             double* sigma, int8_t* flow, uint32_t* flags) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < m.n_faces; f += stride) {
+    const int32_t o = m.face_owner[f], nb = m.face_neighbor[f];
+    const int tag = m.face_tag[f];
+    const bool interior = nb >= 0;
+    double n[3] = {0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) n[i] = m.face_normal[f * DIM + i];
+    sigma[f] = 0.0;
+    flow[f] = interior ? -1 : 0;
+    if (!interior && tag == PDG_TAG_INTERIOR) {
+      raise_flag(flags, PDG_FLAG_UNCLASSIFIED);
+      continue;
+    }
+    if (!interior && tag != PDG_TAG_DIRICHLET) continue;  // inflow/neumann/outflow need neither
+
+    // -- flow side: order-2 sample points of every sub-facet
+    if (C.has_advection) {
+      const int r0 = R.face_offset[2], nq = R.face_count[2];
+      double sum = 0.0, mn = INFINITY, mx = -INFINITY, amax = 0.0;
+      int cnt = 0;
+      for (int64_t row = m.face_ptr[f]; row < m.face_ptr[f + 1]; ++row) {
+        double v0[3], E[3][3];
+        facet_frame<DIM>(m, row, v0, E, flags);
+        for (int k = 0; k < nq; ++k) {
+          const double* xi = R.points + (int64_t)(r0 + k) * 3;
+          double x[3] = {0, 0, 0};
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) {
+            double acc = v0[i];
+#pragma unroll
+            for (int j = 0; j < DIM - 1; ++j) acc += xi[j] * E[j][i];
+            x[i] = acc;
+          }
+          double bn = 0.0;
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) bn += eval_prog(C, C.advection[i], x) * n[i];
+          sum += bn;
+          mn = fmin(mn, bn);
+          mx = fmax(mx, bn);
+          amax = fmax(amax, fabs(bn));
+          ++cnt;
+        }
+      }
+      const double tol = 1e-10 * fmax(1.0, amax);
+      if (mn < -tol && mx > tol) raise_flag(flags, PDG_FLAG_STRADDLE);
+      const double mean = sum / cnt;
+      if (interior) flow[f] = mean < 0.0 ? 0 : (mean > 0.0 ? 1 : -1);
+      else flow[f] = mean < 0.0 ? 1 : 0;
+    }
+
+    // -- penalty
+    double best = 0.0;
+    for (int side = 0; side < (interior ? 2 : 1); ++side) {
+      const int32_t el = side == 0 ? o : nb;
+      double mxv = -1.0;
+      bool any = false;
+      for (int64_t row = m.face_ptr[f]; row < m.face_ptr[f + 1]; ++row) {
+        const int32_t s = side == 0 ? m.facet_owner_simplex[row] : m.facet_neighbor_simplex[row];
+        if (s < 0) continue;
+        const double v = m.simplex_volumes[s];
+        mxv = any ? fmax(mxv, v) : v;
+        any = true;
+      }
+      if (!any || !(mxv > 0.0)) {
+        raise_flag(flags, PDG_FLAG_NO_ADJACENT_SIMPLEX);
+        continue;
+      }
+      const int p = B.degree[el];
+      const double vol = m.elem_volumes[el];
+      double cap = INFINITY;
+      if (prm.coverable && prm.coverable[el]) {
+        double c = 1.0;
+        for (int k = 0; k < 2 * (DIM - 1); ++k) c *= (double)p;
+        cap = c;
+      }
+      const double ab = side_abar<DIM>(m, B, C, R, prm, abar_iso, el, n, flags);
+      const double ratio = fmin(vol / mxv, cap);
+      best = fmax(best, ratio * ab * (double)(p * p) * m.face_measure[f] / vol);
+    }
+    sigma[f] = prm.penalty_constant * best;
+  }
+}
+
+// Interface records (pdg_iface_rec) of the owned rows: one thread per row
+// element walks its sorted neighbour list (assembly.py:309-321: column start
+// = prefix of the neighbours' DoF counts) and flattens, per entry, the
+// interface's first-face metadata the element kernel needs before any face
+// point can be tabulated (face range, side, downwind flag, sigma, normal,
+// first sub-facet row, paired-round eligibility).
+template <int DIM>
+__global__ void iface_records_kernel(const pdg_mesh m, const pdg_basis B, const pdg_rules R, int inc,
+                                     int has_adv, const pdg_pattern P, const double* sigma,
+                                     const int8_t* flow) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < P.n_row_elements; k += stride) {
+    const int32_t e = P.row_elements ? P.row_elements[k] : (int32_t)k;
+    const int pe = B.degree[e];
+    const int64_t q1 = P.nbr_ptr[e + 1];
+    int col = 0;
+    for (int64_t q = P.nbr_ptr[e]; q < q1; ++q) {
+      const int32_t j = P.nbr_elem[q];
+      const int nj = (int)(B.dof_offset[j + 1] - B.dof_offset[j]);
+      const int pj = B.degree[j];
+      int fa = 0, fb = 0, row0 = 0, info = 0;
+      double sig = 0.0, nrm[3] = {0.0, 0.0, 0.0};
+      if (j != e) {
+        const int32_t ifc = P.nbr_iface[q];
+        fa = (int)m.iface_ptr[ifc];
+        fb = (int)m.iface_ptr[ifc + 1];
+        const int side = m.face_owner[fa] == e ? 0 : 1;
+        const bool down = has_adv && flow[fa] == side;
+        row0 = (int)m.face_ptr[fa];
+        const int nrows = (int)(m.face_ptr[fa + 1] - row0);
+        const int nq = R.face_count[2 * max(pe, pj) + inc];
+        const bool simple = fb - fa == 1 && nrows == 1 && nq <= 8;
+        info = side | (down ? 2 : 0) | (simple ? 4 : 0);
+        sig = sigma[fa];
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)fa * DIM + i];
+      }
+      int4* o = reinterpret_cast<int4*>(P.nbr_rec + q);
+      o[0] = make_int4(j, nj, col, pj);
+      o[1] = make_int4(fa, fb, row0, info);
+      double2* od = reinterpret_cast<double2*>(P.nbr_rec + q) + 2;
+      od[0] = make_double2(sig, nrm[0]);
+      od[1] = make_double2(nrm[1], nrm[2]);
+      col += nj;
+    }
+  }
+}
+
+}  // namespace pdg
+
+using namespace pdg;
+
+extern "C" int pdg_iface_records(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                                 const pdg_rules* rules, const pdg_params* params, const pdg_pattern* pattern,
+                                 const double* sigma, const int8_t* face_flow, pdg_stream stream) {
+  PDG_TRY {
+    if (!mesh || !basis || !coeffs || !rules || !params || !pattern || !sigma || !face_flow ||
+        !pattern->nbr_ptr || !pattern->nbr_elem || !pattern->nbr_iface || !pattern->nbr_rec)
+      return fail(PDG_ERR_INVALID, "null argument");
+    if (pattern->n_row_elements <= 0) return PDG_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int grid = grid_for(pattern->n_row_elements, 128);
+    if (mesh->dim == 2)
+      iface_records_kernel<2><<<grid, 128, 0, st>>>(*mesh, *basis, *rules, params->quad_increment,
+                                                    coeffs->has_advection, *pattern, sigma, face_flow);
+    else if (mesh->dim == 3)
+      iface_records_kernel<3><<<grid, 128, 0, st>>>(*mesh, *basis, *rules, params->quad_increment,
+                                                    coeffs->has_advection, *pattern, sigma, face_flow);
+    else
+      return fail(PDG_ERR_UNSUPPORTED, "dim must be 2 or 3");
+    note_launch();
+    PDG_CUDA(cudaGetLastError());
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+extern "C" int pdg_face_prepass(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                                const pdg_rules* rules, const pdg_params* params, double* sigma,
+                                int8_t* face_flow, double* elem_abar, uint32_t* err_flags,
+                                pdg_stream stream) {
+  PDG_TRY {
+    if (!mesh || !basis || !coeffs || !rules || !params || !sigma || !face_flow)
+      return fail(PDG_ERR_INVALID, "null argument");
+    if (mesh->dim != 2 && mesh->dim != 3) return fail(PDG_ERR_UNSUPPORTED, "dim must be 2 or 3");
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool iso_var = coeffs->diffusion_kind == PDG_DIFF_ISO && !coeffs->diffusion[0].is_const;
+    if (iso_var && !elem_abar) return fail(PDG_ERR_INVALID, "elem_abar scratch required");
+    if (mesh->dim == 2) {
+      if (iso_var && mesh->n_elements > 0) {
+        elem_abar_iso<2><<<grid_for_warps(mesh->n_elements, 256), 256, 0, st>>>(
+            *mesh, *basis, *coeffs, *rules, *params, elem_abar, err_flags);
+        note_launch();
+      }
+      if (mesh->n_faces > 0) {
+        face_prepass<2><<<grid_for(mesh->n_faces, 128), 128, 0, st>>>(
+            *mesh, *basis, *coeffs, *rules, *params, elem_abar, sigma, face_flow, err_flags);
+        note_launch();
+      }
+    } else {
+      if (iso_var && mesh->n_elements > 0) {
+        elem_abar_iso<3><<<grid_for_warps(mesh->n_elements, 256), 256, 0, st>>>(
+            *mesh, *basis, *coeffs, *rules, *params, elem_abar, err_flags);
+        note_launch();
+      }
+      if (mesh->n_faces > 0) {
+        face_prepass<3><<<grid_for(mesh->n_faces, 128), 128, 0, st>>>(
+            *mesh, *basis, *coeffs, *rules, *params, elem_abar, sigma, face_flow, err_flags);
+        note_launch();
+      }
+    }
+    PDG_CUDA(cudaGetLastError());
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+// ---------------------------------------------------------------------------
+// geometry pre-pass: affine frames of every simplex (element order), every
+// facet, and the basis constants of every element
+// ---------------------------------------------------------------------------
+namespace pdg {
+
+template <int DIM>
+__global__ void frames_kernel(const pdg_mesh m, const pdg_basis B, const pdg_frames F, uint32_t* flags) {
+  constexpr int W = DIM == 2 ? 8 : 16;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = tid; i < m.n_simplices; i += stride) {
+    double v0[3], E[3][3];
+    const double det = simplex_frame<DIM>(m, m.elem_simplices[i], v0, E, flags);
+    double* o = F.simplex + i * W;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) o[d] = v0[d];
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
+    o[DIM + DIM * DIM] = det;
+    o[DIM + DIM * DIM + 1] = sqrt(det);  // sqrt-weighted volume tables (assemble_body.cuh)
+  }
+  for (int64_t r = tid; r < m.n_facets; r += stride) {
+    double v0[3], E[3][3];
+    const double jac = facet_frame<DIM>(m, r, v0, E, flags);
+    double* o = F.facet + r * W;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) o[d] = v0[d];
+#pragma unroll
+    for (int k = 0; k < DIM - 1; ++k)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
+    o[DIM + (DIM - 1) * DIM] = jac;
+  }
+  for (int64_t e = tid; e < m.n_elements; e += stride) {
+    const BoxConst<DIM> b = box_const<DIM>(B.box + e * 2 * DIM);
+    double* o = F.element + e * W;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      o[d] = b.c[d];
+      o[DIM + d] = b.ih[d];
+      o[2 * DIM + d] = b.rs[d];
+    }
+  }
+}
+
+}  // namespace pdg
+
+extern "C" int pdg_frames_build(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_frames* frames,
+                                uint32_t* err_flags, pdg_stream stream) {
+  PDG_TRY {
+    if (!mesh || !basis || !frames || !frames->simplex || !frames->facet || !frames->element)
+      return fail(PDG_ERR_INVALID, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = std::max(mesh->n_simplices, std::max(mesh->n_facets, mesh->n_elements));
+    if (n == 0) return PDG_OK;
+    if (mesh->dim == 2) frames_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(*mesh, *basis, *frames, err_flags);
+    else if (mesh->dim == 3) frames_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(*mesh, *basis, *frames, err_flags);
+    else return fail(PDG_ERR_UNSUPPORTED, "dim must be 2 or 3");
+    note_launch();
+    PDG_CUDA(cudaGetLastError());
+    return PDG_OK;
+  }
+  PDG_CATCH
+}

@@ -137,6 +137,14 @@ static bool jit_ws() {
   return v && v[0] == '1';
 }
 
+// PDG_JIT_WARPS: warps per CTA of the single-warp body (default 4).  Small CTAs
+// let the register budget, not the CTA granularity, set the resident warp count.
+static int jit_warps() {
+  const char* v = getenv("PDG_JIT_WARPS");
+  const int w = v ? atoi(v) : 4;
+  return w >= 1 && w <= 8 ? w : 4;
+}
+
 static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv) {
   // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow.
   // single-warp body: CTA = 128 threads, default 3 (168 registers, 12 warps/SM;
@@ -149,8 +157,13 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
   os << "#include \"" << (ws ? "assemble_ws.cuh" : "assemble_body.cuh") << "\"\n"
      << "namespace pdg_jit {\nusing namespace pdg;\n"
      << policy << "\n}\n"
-     << "extern \"C\" __global__ void __launch_bounds__(" << (ws ? 64 : 128) << ", " << minblocks
-     << ") pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {\n"
+     << "extern \"C\" __global__ void ";
+  // PDG_JIT_MAXNREG: a register cap (__maxnreg__) instead of the minimum-CTAs bound
+  if (const char* mr = getenv("PDG_JIT_MAXNREG"))
+    os << "__maxnreg__(" << atoi(mr) << ")";
+  else
+    os << "__launch_bounds__(" << (ws ? 64 : 32 * jit_warps()) << ", " << minblocks << ")";
+  os << " pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {\n"
      << "  pdg::" << (ws ? "assemble_ws<" : "assemble_body<") << dim << ", " << P << ", "
      << (sym ? "true" : "false");
   if (!ws) os << ", pdg_jit::JitCoef, " << kv;
@@ -295,7 +308,7 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     a.lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, jit_rhs_regs_max());
     const std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, sym, a.lay.kv, k);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
-    int threads = 128;
+    int threads = 32 * jit_warps();
     size_t smem = (size_t)a.lay.warp_doubles * 8 * (threads / 32);
     if (ws) {  // one producer/consumer pair per CTA: two stages + header + neighbour staging
       int kv = 32;
@@ -309,7 +322,7 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
       return fail(PDG_ERR_CUDA, "cuFuncSetAttribute(max dynamic smem) failed");
     int per_sm = 0;
     if (A.cuOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, threads, smem) != 0 || per_sm < 1) per_sm = 1;
-    const int64_t need = ws ? pattern->n_row_elements : (pattern->n_row_elements + 3) / 4;
+    const int64_t need = ws ? pattern->n_row_elements : (pattern->n_row_elements + threads / 32 - 1) / (threads / 32);
     const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm * (ws ? 1 : 8));
     if (grid <= 0) return PDG_OK;
     void* args[] = {&a};

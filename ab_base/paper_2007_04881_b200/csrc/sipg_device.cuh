@@ -15,6 +15,7 @@
 
 #ifndef __CUDACC_RTC__
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #endif
 

@@ -15,12 +15,14 @@ def main(cfg="cfg5", degree=None, sym=True, minblocks=3, ws="0"):
     p = w.degree if degree is None else int(degree)
     pol = policy_source(coefficients(w.coeffs, w.dim), w.dim)
     body = "assemble_ws" if str(ws) == "1" else "assemble_body"
-    threads = 64 if str(ws) == "1" else 128
+    threads = 64 if str(ws) == "1" else 32 * int(os.environ.get("PDG_JIT_WARPS", "4"))
     sym = str(sym) not in ("0", "False", "false")
+    mr = os.environ.get("PDG_JIT_MAXNREG")
+    bounds = f"__maxnreg__({mr})" if mr else f"__launch_bounds__({threads}, {minblocks})"
+    tail = ", pdg_jit::JitCoef, 32" if body == "assemble_body" else ""
     src = (f'#include "{body}.cuh"\nnamespace pdg_jit {{\nusing namespace pdg;\n' + pol + '\n}\n'
-           f'extern "C" __global__ void __launch_bounds__({threads}, {minblocks}) pdg_jit_kernel('
-           'const __grid_constant__ pdg::KArgs a) {\n'
-           f'  pdg::{body}<{w.dim}, {p}, {"true" if sym else "false"}{", pdg_jit::JitCoef, 32" if body == "assemble_body" else ""}>(a, pdg_jit::JitCoef());\n}}\n')
+           f'extern "C" __global__ void {bounds} pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {{\n'
+           f'  pdg::{body}<{w.dim}, {p}, {"true" if sym else "false"}{tail}>(a, pdg_jit::JitCoef());\n}}\n')
     lib = C.CDLL("libnvrtc.so.12")
     prog = C.c_void_p()
     assert lib.nvrtcCreateProgram(C.byref(prog), src.encode(), b"pdg_jit.cu", 0, None, None) == 0

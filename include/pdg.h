@@ -143,6 +143,8 @@ typedef struct pdg_rules {
   const int32_t* face_offset;  /* [max_order+1] interval (2D) / triangle (3D) rule */
   const int32_t* face_count;
   const double* sqrt_weights;  /* [n] sqrt(weights) (sqrt-weighted symmetric volume tables) */
+  int32_t n_points;            /* n (small tables are staged in shared memory by the kernels) */
+  int32_t pad_;
 } pdg_rules;
 
 typedef struct pdg_params {
@@ -165,7 +167,7 @@ enum {
  * flattened by pdg_iface_records so the element kernel stages a window of
  * neighbours with one contiguous asynchronous copy instead of chains of
  * dependent gathers (nbr -> interface -> face -> sigma / normal / frame).
- * 64 bytes.  Self entry: j == e, fa == fb. */
+ * 80 bytes.  Self entry: j == e, fa == fb. */
 typedef struct pdg_iface_rec {
   int32_t j;        /* neighbour element (sorted ascending, self included) */
   int32_t nj;       /* its number of basis functions */
@@ -177,6 +179,8 @@ typedef struct pdg_iface_rec {
                        bit2: single face, single sub-facet, <= 8 face points (paired rounds) */
   double sig;       /* penalty of face fa (model.py:238-257) */
   double nrm[3];    /* owner normal of face fa */
+  int64_t dof;      /* first global DoF of j (= first column index of its block) */
+  int64_t pad_;
 } pdg_iface_rec;
 
 /* Block pattern of the rows owned by one assembly (assembly.py:209-340). */

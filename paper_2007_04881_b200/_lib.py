@@ -71,7 +71,7 @@ class Coeffs(C.Structure):
 class Rules(C.Structure):
     _fields_ = [("max_order", _i32), ("points", _p), ("weights", _p),
                 ("vol_offset", _p), ("vol_count", _p), ("face_offset", _p), ("face_count", _p),
-                ("sqrt_weights", _p)]
+                ("sqrt_weights", _p), ("n_points", _i32), ("pad_", _i32)]
 
 
 class Params(C.Structure):

@@ -329,6 +329,7 @@ class DeviceRules:
         r.vol_offset, r.vol_count = _lib.ptr(self.t["vo"]), _lib.ptr(self.t["vn"])
         r.face_offset, r.face_count = _lib.ptr(self.t["fo"]), _lib.ptr(self.t["fn"])
         r.sqrt_weights = _lib.ptr(self.t["sqrt_weights"])
+        r.n_points = int(table.weights.size)
         self.struct = r
 
 
@@ -451,7 +452,7 @@ class SipgPlan:
         self.t.update(nbr_ptr=z(nel + 1, i64), nbr_elem=z(nadj, i32), nbr_iface=z(nadj, i32),
                       row_len=z(nr, i64), val_off=z(nr + 1, i64), row_off=z(nr + 1, i64),
                       row_ptr=z(self.n_local_rows + 1, i64),
-                      nbr_rec=z(nadj * 8, torch.float64),  # pdg_iface_rec, 64 B per entry
+                      nbr_rec=z(nadj * 10, torch.float64),  # pdg_iface_rec, 80 B per entry
                       sigma=z(flat.n_faces, torch.float64), flow=z(flat.n_faces, torch.int8),
                       abar=z(nel, torch.float64), flags=torch.zeros(1, dtype=torch.int32, device=dev))
         W = 8 if d == 2 else 16

@@ -57,10 +57,51 @@ namespace pdg {
 #define PDG_FACE_UNROLL 1
 #endif
 
+// phase timers (diagnostics: one warp prints its clock64 split at exit)
+#ifndef PDG_TIMERS
+#define PDG_TIMERS 0
+#endif
+#define PDG_T(i)                                 \
+  if (PDG_TIMERS) {                              \
+    const long long now_ = clock64();            \
+    tacc[i] += now_ - tprev;                     \
+    tprev = now_;                                \
+  }
+
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
 constexpr int NBR_WIN = 16;  // neighbour entries staged per window
 constexpr int FR_MAX = 32;   // simplex frames of one element kept in shared memory
+constexpr int REC16 = (int)(sizeof(pdg_iface_rec) / 16);  // 16-byte chunks per interface record
+constexpr int RULE_SMEM_MAX = 128;  // rule tables up to this many points live in shared memory (per CTA)
+#ifndef PDG_RULES_SMEM
+#define PDG_RULES_SMEM 1
+#endif
+
+// doubles of the per-CTA rule copy (points [n][3], weights [n], sqrt weights [n]), 0 if not staged
+inline __host__ __device__ int rule_smem_doubles(int n_points) {
+  return (n_points > 0 && n_points <= RULE_SMEM_MAX) ? ((5 * n_points + 1) & ~1) : 0;
+}
+
+// the quadrature tables a kernel reads: the CTA's shared copy when staged
+struct RuleView {
+  const double* pts;  // [n][3]
+  const double* w;    // [n]
+  const double* sw;   // [n]
+};
+
+// stage the rule tables into the CTA's shared memory (all threads; ends with a CTA barrier)
+__device__ __forceinline__ RuleView stage_rules(const pdg_rules& R, double* sm) {
+  const int n = R.n_points;
+  if (!PDG_RULES_SMEM || n <= 0 || n > RULE_SMEM_MAX) return RuleView{R.points, R.weights, R.sqrt_weights};
+  for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) sm[i] = R.points[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sm[3 * n + i] = R.weights[i];
+    sm[4 * n + i] = R.sqrt_weights[i];
+  }
+  __syncthreads();
+  return RuleView{sm, sm + 3 * n, sm + 4 * n};
+}
 
 template <int DIM>
 struct Widths {
@@ -233,7 +274,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   const pdg_pattern& pat = a.pat;
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  double* buf = smem + (threadIdx.x >> 5) * a.lay.warp_doubles;
+  const RuleView RV = stage_rules(R, smem);
+  double* buf = smem + rule_smem_doubles(PDG_RULES_SMEM ? R.n_points : 0) + (threadIdx.x >> 5) * a.lay.warp_doubles;
   double* sc1 = buf + a.lay.buf_doubles;
   double* sc2 = sc1 + 32;
   // interface records of the current / next element's first neighbour window
@@ -270,7 +312,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       const int nwn = min(NBR_WIN, (int)(pat.nbr_ptr[en + 1] - r0n));
       const double* rsrc = reinterpret_cast<const double*>(pat.nbr_rec + r0n);
       double* rdst = reinterpret_cast<double*>(recs + rb * NBR_WIN);
-      for (int c = lane; c < nwn * 4; c += 32) cp_async16(rdst + 2 * c, rsrc + 2 * c);
+      for (int c = lane; c < nwn * REC16; c += 32) cp_async16(rdst + 2 * c, rsrc + 2 * c);
     }
     const int64_t s0n = m.elem_ptr[en];
     const int nsn = (int)(m.elem_ptr[en + 1] - s0n);
@@ -290,6 +332,9 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   int rb = 0;
   bool next_frames = issue_next(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, rb);
   cp_async_commit();
+  long long tacc[PDG_TIMERS ? 9 : 1] = {0};
+  long long tprev = PDG_TIMERS ? clock64() : 0;
+  int nel_done = 0;
   for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < pat.n_row_elements;
        k += nwarps, rb ^= 1) {
     const bool fr_smem = next_frames;
@@ -321,6 +366,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       else rhs_s[f * 32 + lane] += v;
     };
 
+    ++nel_done;
+    PDG_T(0)
     // ------------------------------------------------------------ volume
     {
       const int order = 2 * pe + a.prm.quad_increment;
@@ -334,18 +381,18 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           const double valid = lane < nvalid ? 1.0 : 0.0;
           const int ls = gq / nq;
           const int kq = gq - ls * nq;
-          const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+          const double* xi = RV.pts + (r0 + kq) * 3;
           double x[3] = {0.0, 0.0, 0.0};
           const double* fr = fr_smem ? sfr + ls * W::SF : a.sframe + (s0 + ls) * W::SF;
           const double det = frame_point<DIM, DIM>(fr, xi, x);
-          const double w = R.weights[r0 + kq] * det * valid;
+          const double w = RV.w[r0 + kq] * det * valid;
           Tab<DIM, P> tb;
           tb.load(bx, x);
           double* col = buf + lane;
           if (nG && sqrtw) {
             const double av = cf.a_iso(x);
             if (av < 0.0) raise_flag(a.flags, PDG_FLAG_NEG_DIFFUSION);
-            const double sw = R.sqrt_weights[r0 + kq] * fr[DIM + DIM * DIM + 1] * sqrt(fmax(av, 0.0)) * valid;
+            const double sw = RV.sw[r0 + kq] * fr[DIM + DIM * DIM + 1] * sqrt(fmax(av, 0.0)) * valid;
             Tab<DIM, P> ts = tb;
             ts.scale(sw);
 #pragma unroll
@@ -406,6 +453,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           }
         }
         __syncwarp();
+        PDG_T(1)
         const int nk = (nvalid + 3) >> 2;
         auto vol_kstep = [&](int kk) {
           const int q = kk * 4 + t;
@@ -464,6 +512,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           for (int kk = 0; kk < nk; ++kk) vol_kstep(kk);
         }
         __syncwarp();
+        PDG_T(2)
       }
     }
 
@@ -489,10 +538,10 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
     // tabulate one face slot: own trace (lanes 0-15) or neighbour trace (16-31)
     auto tab_slot = [&](const double* nrm, const double* frp, int r0, int kq, double valid, double sig, double sgn,
                         bool down, const BoxConst<DIM>& bo) {
-      const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+      const double* xi = RV.pts + (r0 + kq) * 3;
       double x[3] = {0.0, 0.0, 0.0};
       const double jac = frame_point<DIM, DIM - 1>(frp, xi, x);
-      const double w = R.weights[r0 + kq] * jac * valid;
+      const double w = RV.w[r0 + kq] * jac * valid;
       Tab<DIM, P> tb;
       tb.load(mine ? bx : bo, x);
       double av = 1.0;
@@ -567,6 +616,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       }
     };
 
+    PDG_T(3)
     for (int w0 = 0; w0 < nnb; w0 += NBR_WIN) {
       const int nw = min(NBR_WIN, nnb - w0);
       if (w0 == 0) {
@@ -576,7 +626,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         // windows beyond the first (more than NBR_WIN neighbours): synchronous restage
         __syncwarp();
         const double* rsrc = reinterpret_cast<const double*>(pat.nbr_rec + q0 + w0);
-        for (int c = lane; c < nw * 4; c += 32) cp_async16(reinterpret_cast<double*>(rc) + 2 * c, rsrc + 2 * c);
+        for (int c = lane; c < nw * REC16; c += 32) cp_async16(reinterpret_cast<double*>(rc) + 2 * c, rsrc + 2 * c);
         cp_async_commit();
         cp_async_wait_all();
         __syncwarp();
@@ -596,11 +646,13 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         int q = 0;
         for (int p = c0 + lane; p < c1; p += 32) {
           while (q + 1 < nw && rc[q + 1].col <= p) ++q;
-          const int64_t cv = B.dof_offset[rc[q].j] + (p - rc[q].col);
+          const int64_t cv = rc[q].dof + (p - rc[q].col);
           int64_t* dst = pat.col_idx + voff + p;
+#pragma unroll 4
           for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
         }
       }
+      PDG_T(4)
       int qi = 0;
       while (qi < nw) {
         if (rc[qi].j == e) {
@@ -627,12 +679,14 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           tab_slot(nrm, ffr + q * W::FF, r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, rc[q].sig,
                    (info & 1) ? -1.0 : 1.0, (info & 2) != 0, bo);
           __syncwarp();
+          PDG_T(5)
           face_contract(0, 2, co);
           store_block<NT, false>(a.values, voff, Lrow, rc[qi].col, ne, rc[qi].nj, co, g, t);
           zero_tiles<NT>(co);
           face_contract(2, 4, co);
           store_block<NT, false>(a.values, voff, Lrow, rc[qb].col, ne, rc[qb].nj, co, g, t);
           __syncwarp();
+          PDG_T(6)
           qi = qb + 1;
           continue;
         }
@@ -683,6 +737,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       __syncwarp();
     }
 
+    PDG_T(4)
     // ------------------------------------------------------------ boundary faces
     const int64_t bend = mode ? 0 : m.elem_bface_ptr[e + 1];
     for (int64_t bi = mode ? 0 : m.elem_bface_ptr[e]; bi < bend; ++bi) {
@@ -710,10 +765,10 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           const double valid = (slot < nvalid && mine) ? 1.0 : 0.0;
           const int lr = gq / nq;
           const int kq = gq - lr * nq;
-          const double* xi = R.points + (int64_t)(r0 + kq) * 3;
+          const double* xi = RV.pts + (r0 + kq) * 3;
           double x[3] = {0.0, 0.0, 0.0};
           const double jac = frame_point<DIM, DIM - 1>(a.fframe + (row0 + lr) * W::FF, xi, x);
-          const double w = R.weights[r0 + kq] * jac * valid;
+          const double w = RV.w[r0 + kq] * jac * valid;
           Tab<DIM, P> tb;
           tb.load(bx, x);
           double av = 1.0;
@@ -796,6 +851,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       }
     }
 
+    PDG_T(7)
     // ------------------------------------------------------------ write-out
     store_block<NT, SYM>(a.values, voff, Lrow, colself, ne, ne, cd, g, t);
     double* rhs_out = mode ? a.rhs + k * NB : a.rhs + dof_e;
@@ -818,6 +874,14 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       }
     }
     __syncwarp();
+    PDG_T(8)
+  }
+  if (PDG_TIMERS && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && threadIdx.x < 64) {
+    const double n = nel_done > 0 ? nel_done : 1;
+    printf("PDG_TIMERS blk %d warp %d elements %d per-element cycles: start %.0f voltab %.0f volmma %.0f post %.0f "
+           "window %.0f facetab %.0f facemma %.0f boundary %.0f writeout %.0f\n",
+           blockIdx.x, threadIdx.x >> 5, nel_done, tacc[0] / n, tacc[1] / n, tacc[2] / n, tacc[3] / n, tacc[4] / n,
+           tacc[5] / n, tacc[6] / n, tacc[7] / n, tacc[8] / n);
   }
 }
 

@@ -52,7 +52,8 @@ template <int DIM, int P, bool SYM>
 cudaError_t launch_assemble(KArgs a, const pdg_coeffs& C, cudaStream_t st) {
   a.lay = make_layout(DIM, P, C.diffusion_kind, C.has_advection || C.has_reaction);
   const int threads = 128;
-  const size_t smem = (size_t)a.lay.warp_doubles * 8 * (threads / 32);
+  const size_t smem = ((size_t)rule_smem_doubles(PDG_RULES_SMEM ? a.R.n_points : 0) +
+                       (size_t)a.lay.warp_doubles * (threads / 32)) * 8;
   auto kern = assemble_elements<DIM, P, SYM>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;

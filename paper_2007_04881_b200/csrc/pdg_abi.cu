@@ -137,7 +137,7 @@ static cudaError_t launch_tabulate(int P, const pdg_basis& B, int32_t el, const 
 
 using namespace pdg;
 
-static_assert(sizeof(pdg_iface_rec) == 64, "pdg_iface_rec is a 64-byte record");
+static_assert(sizeof(pdg_iface_rec) == 80, "pdg_iface_rec is an 80-byte record");
 
 extern "C" int pdg_abi_version(void) { return PDG_ABI_VERSION; }
 

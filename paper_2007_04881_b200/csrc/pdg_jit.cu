@@ -309,7 +309,8 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     const std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, sym, a.lay.kv, k);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
     int threads = 32 * jit_warps();
-    size_t smem = (size_t)a.lay.warp_doubles * 8 * (threads / 32);
+    // the CTA's rule copy (always reserved: the JIT build may toggle PDG_RULES_SMEM)
+    size_t smem = ((size_t)rule_smem_doubles(rules->n_points) + (size_t)a.lay.warp_doubles * (threads / 32)) * 8;
     if (ws) {  // one producer/consumer pair per CTA: two stages + header + neighbour staging
       int kv = 32;
       a.lay.buf_doubles = ws_table_doubles(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, &kv);

@@ -243,6 +243,7 @@ __global__ void iface_records_kernel(const pdg_mesh m, const pdg_basis B, const 
       double2* od = reinterpret_cast<double2*>(P.nbr_rec + q) + 2;
       od[0] = make_double2(sig, nrm[0]);
       od[1] = make_double2(nrm[1], nrm[2]);
+      reinterpret_cast<longlong2*>(P.nbr_rec + q)[4] = make_longlong2(B.dof_offset[j], 0);
       col += nj;
     }
   }
