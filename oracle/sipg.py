@@ -110,7 +110,17 @@ def graded_lex(p: int, d: int) -> np.ndarray:
     return np.array(rows, dtype=np.int64).reshape(-1, d)
 
 
-def tabulate(degree: int, box, pts):
+@lru_cache(maxsize=None)
+def multi_indices(p: int, d: int, family: str = "P") -> np.ndarray:
+    """basis.py:93-104: family P = graded lex; family PQ (space-time) = spatial
+    graded-lex multi-index of degree <= p times time degree k <= p, time outer."""
+    if family == "P":
+        return graded_lex(p, d)
+    sp = graded_lex(p, d - 1)
+    return np.array([(*a, k) for k in range(p + 1) for a in sp], dtype=np.int64).reshape(-1, d)
+
+
+def tabulate(degree: int, box, pts, family: str = "P"):
     """basis.py:107-164: orthonormal box Legendre values (n,q) + grads (n,d,q)."""
     pts = np.atleast_2d(np.asarray(pts, float))
     box = np.asarray(box, float)
@@ -133,7 +143,7 @@ def tabulate(degree: int, box, pts):
         s = nrm / np.sqrt(hi[i] - lo[i])
         v1[i] = L * s[:, None]
         g1[i] = dL * (s / half[i])[:, None]
-    al = graded_lex(p, d)
+    al = multi_indices(p, d, family)
     dims = np.arange(d)[None, :]
     fv = v1[dims, al, :]                       # (n, d, q)
     vals = fv.prod(axis=1)
@@ -148,10 +158,15 @@ def tabulate(degree: int, box, pts):
 
 # -- kernel mathematics (assembly.py:396-512) ----------------------------------------
 
-def volume_block(deg, box, pts, w, C):
+def _tab(sp, pts):
+    """sp = (degree, box[, family])."""
+    return tabulate(sp[0], sp[1], pts, sp[2] if len(sp) > 2 else "P")
+
+
+def volume_block(deg, box, pts, w, C, family="P"):
     """assembly.py:396-415: K_ij = sum_q w (A grad phi_j).grad phi_i + (b.grad phi_j) phi_i
     + c phi_j phi_i;  load_i = sum_q w f phi_i."""
-    V, G = tabulate(deg, box, pts)
+    V, G = tabulate(deg, box, pts, family)
     K = np.zeros((V.shape[0], V.shape[0]))
     if C.diffusion is not None:
         AG = np.einsum("qab,nbq->naq", C.diffusion(pts), G)
@@ -166,8 +181,8 @@ def volume_block(deg, box, pts, w, C):
 
 def interior_blocks(sp_o, sp_n, pts, w, nrm, C, sigma, upwind, grad_terms=True):
     """assembly.py:418-463: blocks [[oo, on], [no, nn]] of one interior sub-facet."""
-    Vo, Go = tabulate(sp_o[0], sp_o[1], pts)
-    Vn, Gn = tabulate(sp_n[0], sp_n[1], pts)
+    Vo, Go = _tab(sp_o, pts)
+    Vn, Gn = _tab(sp_n, pts)
     V = (Vo, Vn)
     s = (1.0, -1.0)
     B = [[np.zeros((V[a].shape[0], V[b].shape[0])) for b in range(2)] for a in range(2)]
@@ -195,7 +210,7 @@ def interior_blocks(sp_o, sp_n, pts, w, nrm, C, sigma, upwind, grad_terms=True):
 
 def dirichlet_block(sp, pts, w, nrm, C, sigma, with_inflow, grad_terms=True):
     """assembly.py:466-493."""
-    V, G = tabulate(sp[0], sp[1], pts)
+    V, G = _tab(sp, pts)
     n = V.shape[0]
     K, f = np.zeros((n, n)), np.zeros(n)
     g = C.dirichlet_data(pts) if C.dirichlet_data is not None else None
@@ -218,19 +233,21 @@ def dirichlet_block(sp, pts, w, nrm, C, sigma, with_inflow, grad_terms=True):
     return K, f
 
 
-def inflow_block(sp, pts, w, nrm, C):
-    """assembly.py:496-505 (boundary values = dirichlet_data, assembly.py:628-631)."""
-    V, _ = tabulate(sp[0], sp[1], pts)
+def inflow_block(sp, pts, w, nrm, C, g="dirichlet"):
+    """assembly.py:496-505 (boundary values = geom.inflow_values: dirichlet_data,
+    assembly.py:628-631, or the previous slab's trace, spacetime.py:355-362)."""
+    V, _ = _tab(sp, pts)
     wbn = w * (C.advection(pts) @ nrm)
     K = -np.einsum("q,jq,iq->ij", wbn, V, V)
-    g = C.dirichlet_data(pts) if C.dirichlet_data is not None else None
+    if isinstance(g, str):
+        g = C.dirichlet_data(pts) if C.dirichlet_data is not None else None
     f = np.zeros(V.shape[0]) if g is None else -(V @ (wbn * g))
     return K, f
 
 
 def neumann_load(sp, pts, w, C):
     """assembly.py:508-512."""
-    V, _ = tabulate(sp[0], sp[1], pts)
+    V, _ = _tab(sp, pts)
     if C.neumann_data is None:
         return np.zeros(V.shape[0])
     return V @ (w * C.neumann_data(pts))

@@ -186,3 +186,54 @@ def hyperbolic(dim):
     b = [M.const(1.0), M.const(0.5)] + ([M.const(0.25)] if dim == 3 else [])
     return M.PdeCoefficients(advection=M.VectorField(b), reaction=M.constant_scalar(1.0),
                              source=M.ScalarField(1.0 + X), dirichlet_data=M.ScalarField(Y))
+
+
+# ---- space-time slab coefficient sets (coordinates (x, y, t), time last) ----
+# the block form of polydg's parabolic problems (model.py:263-303):
+# diffusion [[a, 0], [0, 0]], advection (w, 1)
+
+T = M.Z
+
+
+def slab_heat():
+    """polydg parabolic_sine_problem (model.py:277-303): u = sin(pi x) sin(pi y) (1 - t)."""
+    pi = np.pi
+    s = M.sin(pi * X) * M.sin(pi * Y)
+    coeffs = M.PdeCoefficients(
+        diffusion=M.constant_tensor(np.diag([1.0, 1.0, 0.0])),
+        advection=M.constant_vector([0.0, 0.0, 1.0]),
+        reaction=M.constant_scalar(1.0),
+        source=M.ScalarField(s * ((2.0 * pi ** 2 + 1.0) * (1.0 - T) - 1.0)),
+        dirichlet_data=M.ScalarField(s * (1.0 - T)))
+    return coeffs, M.ScalarField(s)
+
+
+def slab_adv_heat():
+    """Variable spatial diffusion, oblique transport (lateral upwinding and
+    inflow Dirichlet faces), Neumann data on x >= 0.5."""
+    a = 0.1 * (1.0 + 0.5 * X)
+    z = 0.0 * X
+    coeffs = M.PdeCoefficients(
+        diffusion=M.TensorField(3, entries=[a, z, z, z, a, z, z, z, z]),
+        advection=M.constant_vector([0.5, 0.25, 1.0]),
+        source=M.ScalarField(1.0 + T * X),
+        dirichlet_data=M.ScalarField(X + T),
+        neumann_data=M.ScalarField(1.0 + Y))
+    return coeffs, M.ScalarField(X * Y)
+
+
+def slab_transport():
+    """No diffusion: lateral boundary faces are inflow / outflow."""
+    coeffs = M.PdeCoefficients(
+        advection=M.constant_vector([1.0, 0.5, 1.0]),
+        reaction=M.constant_scalar(0.5),
+        source=M.ScalarField(X + T),
+        dirichlet_data=M.ScalarField(Y))
+    return coeffs, M.ScalarField(1.0 + X)
+
+
+def slab_predicate(name):
+    """Dirichlet/Neumann split of the lateral boundary (None = all Dirichlet)."""
+    if name == "slab_adv_heat":
+        return lambda p: bool(p[0] < 0.5)
+    return None
