@@ -213,6 +213,21 @@ typedef struct pdg_frames {
   double* element;
 } pdg_frames;
 
+/* One space-time slab (polydg spacetime.py:84-104, 133-388): the spatial mesh
+ * x (t0, t1), with prism bases (pdg_basis.box is [n_elements][2][3], time
+ * last) and the time-jump data of the bottom facets. */
+typedef struct pdg_slab {
+  double t0, t1;
+  const int8_t* lateral_tag;      /* [n_faces] PDG_TAG_* of the lateral boundary faces
+                                     (SlabGeometry._classify_lateral, spacetime.py:229-246) */
+  const double* prev_values;      /* previous slab's coefficient vector, or NULL: the initial
+                                     data field of the policy (spacetime.py:367-388) */
+  const int64_t* prev_dof_offset; /* [n_elements+1] previous slab DofMap (same degree/family) */
+  const double* prev_box;         /* [n_elements][2][3] previous slab prism boxes */
+  int32_t family;                 /* basis family of the slab: 0 = P, 1 = PQ (basis.py:21-26) */
+  int32_t table_rows;             /* shared table rows of the coefficient set (model.slab_policy) */
+} pdg_slab;
+
 #ifndef __CUDACC_RTC__ /* the runtime-compiled kernels need the types only */
 int pdg_abi_version(void);
 const char* pdg_last_error(void);
@@ -291,6 +306,36 @@ int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coe
  * use; lets callers pay the NVRTC cost outside timed regions. */
 int pdg_jit_prepare(const pdg_coeffs* coeffs, const char* policy_source, int32_t dim,
                     int32_t max_degree);
+
+/* ---- space-time slabs (polydg spacetime.py; runtime-specialised, NVRTC) ----
+ * The index phase is shared with the spatial path (pdg_adjacency /
+ * pdg_pattern_offsets with the slab basis), as are the spatial affine frames
+ * (pdg_frames_build).  policy_source: model.slab_policy (coefficients in
+ * (x, y, t) + initial data).  Spatial dimension 2 (prisms in 3D), degree
+ * <= PDG_SLAB_MAX_DEGREE, uniform degree for family PQ. */
+#define PDG_SLAB_MAX_DEGREE 4
+
+/* Compile (or fetch) the slab kernels of one coefficient set / degree / family. */
+int pdg_slab_prepare(const char* policy_source, int32_t max_degree, int32_t family);
+
+/* Lateral face pre-pass: penalty sigma with the slab's side data
+ * (spacetime.py:301-351) and the flow side (spacetime.py:287-309) of every
+ * spatial face; replaces SlabGeometry.face_sigma / upwind_side /
+ * dirichlet_inflow. */
+int pdg_slab_prepass(const pdg_mesh* mesh, const pdg_basis* basis, const char* policy_source,
+                     const pdg_rules* rules, const pdg_params* params, const pdg_slab* slab,
+                     const pdg_frames* frames, double* sigma, int8_t* face_flow,
+                     uint32_t* err_flags, pdg_stream stream);
+
+/* Slab element kernel: every owned prism writes its n_e CSR rows (values and
+ * col_idx) and its RHS segment: volume, lateral faces, bottom facet
+ * (replaces assemble_slab's _assemble_approach2 over SlabGeometry,
+ * spacetime.py:391-413). */
+int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, const char* policy_source,
+                      const pdg_rules* rules, const pdg_params* params, const pdg_slab* slab,
+                      const pdg_pattern* pattern, const pdg_frames* frames, const double* sigma,
+                      const int8_t* face_flow, double* values, double* rhs, uint32_t* err_flags,
+                      pdg_stream stream);
 
 /* ---- unit-level entry points (tests / debugging) ---- */
 

@@ -90,10 +90,18 @@ class Frames(C.Structure):
     _fields_ = [("simplex", _p), ("facet", _p), ("element", _p)]
 
 
+class Slab(C.Structure):
+    _fields_ = [("t0", _f64), ("t1", _f64), ("lateral_tag", _p), ("prev_values", _p),
+                ("prev_dof_offset", _p), ("prev_box", _p), ("family", _i32), ("table_rows", _i32)]
+
+
+SLAB_MAX_DEGREE = 4  # include/pdg.h PDG_SLAB_MAX_DEGREE
+
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
 EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes", "pdg_adjacency",
            "pdg_pattern_offsets", "pdg_pattern_fill", "pdg_face_prepass", "pdg_iface_records", "pdg_frames_build",
            "pdg_assemble", "pdg_assemble_jit", "pdg_jit_prepare",
+           "pdg_slab_prepare", "pdg_slab_prepass", "pdg_slab_assemble",
            "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks")
 
 
@@ -128,6 +136,11 @@ def load():
     lib.pdg_assemble_jit.argtypes = [P(Mesh), P(Basis), P(Coeffs), C.c_char_p, P(Rules), P(Params),
                                      P(Pattern), P(Frames), _p, _p, _p, _i32, _p, _p, _p]
     lib.pdg_jit_prepare.argtypes = [P(Coeffs), C.c_char_p, _i32, _i32]
+    lib.pdg_slab_prepare.argtypes = [C.c_char_p, _i32, _i32]
+    lib.pdg_slab_prepass.argtypes = [P(Mesh), P(Basis), C.c_char_p, P(Rules), P(Params), P(Slab),
+                                     P(Frames), _p, _p, _p, _p]
+    lib.pdg_slab_assemble.argtypes = [P(Mesh), P(Basis), C.c_char_p, P(Rules), P(Params), P(Slab),
+                                      P(Pattern), P(Frames), _p, _p, _p, _p, _p, _p]
     lib.pdg_map_simplices.argtypes = [P(Mesh), P(Rules), _i32, _p, _i64, _p, _p, _p, _p]
     lib.pdg_tabulate.argtypes = [P(Mesh), P(Basis), _i32, _p, _i64, _p, _p, _p]
     lib.pdg_element_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params),

@@ -198,19 +198,6 @@ __device__ __forceinline__ BoxConst<DIM> load_box(const double* erec, int64_t e)
   return b;
 }
 
-// x = v0 + xi E from a frame record (v0 then E rows), returns the stored measure
-template <int DIM, int K>
-__device__ __forceinline__ double frame_point(const double* fr, const double* xi, double* x) {
-#pragma unroll
-  for (int i = 0; i < DIM; ++i) {
-    double acc = fr[i];
-#pragma unroll
-    for (int j = 0; j < K; ++j) acc += xi[j] * fr[DIM + j * DIM + i];
-    x[i] = acc;
-  }
-  return fr[DIM + K * DIM];
-}
-
 // Store one C tile set into rows of the element's row block (optionally
 // with its mirror image for symmetric accumulation).
 template <int NT, bool SYM>

@@ -29,6 +29,7 @@
 
 #include "assemble_kernel.cuh"
 #include "assemble_ws.cuh"
+#include "slab_body.cuh"
 
 namespace pdg {
 
@@ -180,12 +181,11 @@ static bool read_file(const std::string& path, std::string& out) {
   return true;
 }
 
-// compile or fetch; returns empty string on success, else the error
-static std::string get_kernel(const std::string& policy, int dim, int P, bool sym, int kv, JitKernel& out) {
+// compile (NVRTC, sm_100a) or fetch a module; returns empty string on success, else the error
+static std::string get_module(const std::string& src, CUmod& out) {
   Api& A = api();
   if (!A.ok) return "JIT unavailable: " + A.why;
   const std::string dir = lib_dir();
-  const std::string src = full_source(policy, dim, P, sym, kv);
   std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
                                    "-DPDG_RHS_REGS_MAX=" + std::to_string(jit_rhs_regs_max()),
                                    "-I" + dir + "/csrc",
@@ -202,7 +202,7 @@ static std::string get_kernel(const std::string& policy, int dim, int P, bool sy
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_cache.find(key);
     if (it != g_cache.end()) {
-      out = it->second;
+      out = it->second.mod;
       return "";
     }
   }
@@ -256,13 +256,25 @@ static std::string get_kernel(const std::string& policy, int dim, int P, bool sy
   cudaFree(nullptr);  // make sure the runtime's primary context is current
   JitKernel k;
   if (A.cuModuleLoadData(&k.mod, cubin.data()) != 0) return "cuModuleLoadData failed";
-  if (A.cuModuleGetFunction(&k.fn, k.mod, "pdg_jit_kernel") != 0) return "cuModuleGetFunction failed";
   {
     std::lock_guard<std::mutex> lk(g_mu);
     g_cache[key] = k;
   }
-  out = k;
+  out = k.mod;
   return "";
+}
+
+static std::string get_function(CUmod mod, const char* name, CUfunc& fn) {
+  if (api().cuModuleGetFunction(&fn, mod, name) != 0) return std::string("cuModuleGetFunction failed: ") + name;
+  return "";
+}
+
+static std::string get_kernel(const std::string& policy, int dim, int P, bool sym, int kv, JitKernel& out) {
+  CUmod mod = nullptr;
+  std::string err = get_module(full_source(policy, dim, P, sym, kv), mod);
+  if (!err.empty()) return err;
+  out.mod = mod;
+  return get_function(mod, "pdg_jit_kernel", out.fn);
 }
 
 KArgs make_kargs(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_rules* rules, const pdg_params* params,
@@ -330,6 +342,153 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     if (A.cuLaunchKernel(k.fn, (unsigned)grid, 1, 1, threads, 1, 1, (unsigned)smem, (cudaStream_t)stream, args,
                          nullptr) != 0)
       return fail(PDG_ERR_CUDA, "cuLaunchKernel failed");
+    note_launch();
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+// ---------------------------------------------------------------------------
+// space-time slabs (slab_body.cuh): one module per (coefficient set, degree,
+// family) holding the slab element kernel and the lateral face pre-pass
+// ---------------------------------------------------------------------------
+namespace pdg {
+
+// PDG_SLAB_WARPS: warps per CTA of the slab kernel (1, 2 or 4; default 4)
+static int slab_warps() {
+  const char* v = getenv("PDG_SLAB_WARPS");
+  const int w = v ? atoi(v) : 4;
+  return (w == 1 || w == 2 || w == 4) ? w : 4;
+}
+
+static int slab_nb(int P, int fam) { return fam ? (P + 1) * binom(P + 2, 2) : binom(P + 3, 3); }
+
+static std::string slab_source(const std::string& policy, int P, int fam, int nw) {
+  std::ostringstream os;
+  os << "#include \"slab_body.cuh\"\n"
+     << "namespace pdg_jit {\nusing namespace pdg;\n" << policy << "\n}\n"
+     << "extern \"C\" __global__ void __launch_bounds__(" << 32 * nw << ", 1) "
+     << "pdg_slab_kernel(const __grid_constant__ pdg::SlabArgs a) {\n"
+     << "  pdg::slab_body<" << P << ", " << (fam ? "true" : "false") << ", " << nw
+     << ", pdg_jit::JitCoef>(a, pdg_jit::JitCoef());\n}\n"
+     << "extern \"C\" __global__ void __launch_bounds__(128) "
+     << "pdg_slab_prepass(const __grid_constant__ pdg::SlabArgs a, double* sigma, int8_t* flow) {\n"
+     << "  pdg::slab_prepass_body(a, pdg_jit::JitCoef(), sigma, flow);\n}\n";
+  return os.str();
+}
+
+static std::string slab_module(const char* policy, int P, int fam, CUmod& mod) {
+  if (P < 0 || P > PDG_SLAB_MAX_DEGREE)
+    return "slab degree " + std::to_string(P) + " outside the supported range 0.." +
+           std::to_string(PDG_SLAB_MAX_DEGREE);
+  return get_module(slab_source(policy, P, fam, slab_warps()), mod);
+}
+
+static int slab_check(const pdg_mesh* mesh, const pdg_basis* basis, const char* policy, const pdg_rules* rules,
+                      const pdg_params* params, const pdg_slab* slab) {
+  if (!mesh || !basis || !policy || !rules || !params || !slab) return fail(PDG_ERR_INVALID, "null argument");
+  if (mesh->dim != 2) return fail(PDG_ERR_UNSUPPORTED, "slabs need a 2D spatial mesh (prisms in 3D)");
+  if (!slab->lateral_tag) return fail(PDG_ERR_INVALID, "lateral tags missing");
+  if (slab->table_rows < 4 || slab->table_rows > 8) return fail(PDG_ERR_INVALID, "table_rows must be 4..8");
+  if (!(slab->t1 > slab->t0)) return fail(PDG_ERR_INVALID, "slab interval must have positive length");
+  if (slab->prev_values && (!slab->prev_dof_offset || !slab->prev_box))
+    return fail(PDG_ERR_INVALID, "previous slab data incomplete");
+  return PDG_OK;
+}
+
+static SlabArgs slab_args(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_rules* rules,
+                          const pdg_params* params, const pdg_slab* slab, const pdg_frames* frames,
+                          const double* sigma, const int8_t* flow, uint32_t* flags) {
+  SlabArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.m = *mesh;
+  a.B = *basis;
+  a.R = *rules;
+  a.prm = *params;
+  a.sl = *slab;
+  a.sframe = frames->simplex;
+  a.fframe = frames->facet;
+  a.sigma = sigma;
+  a.flow = flow;
+  a.flags = flags;
+  return a;
+}
+
+}  // namespace pdg
+
+extern "C" int pdg_slab_prepare(const char* policy_source, int32_t max_degree, int32_t family) {
+  PDG_TRY {
+    if (!policy_source) return fail(PDG_ERR_INVALID, "null argument");
+    CUmod mod = nullptr;
+    const std::string err = slab_module(policy_source, max_degree, family, mod);
+    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+extern "C" int pdg_slab_prepass(const pdg_mesh* mesh, const pdg_basis* basis, const char* policy_source,
+                                const pdg_rules* rules, const pdg_params* params, const pdg_slab* slab,
+                                const pdg_frames* frames, double* sigma, int8_t* face_flow, uint32_t* err_flags,
+                                pdg_stream stream) {
+  PDG_TRY {
+    int rc = slab_check(mesh, basis, policy_source, rules, params, slab);
+    if (rc) return rc;
+    if (!frames || !frames->simplex || !frames->facet || !sigma || !face_flow)
+      return fail(PDG_ERR_INVALID, "null argument");
+    if (mesh->n_faces == 0) return PDG_OK;
+    CUmod mod = nullptr;
+    std::string err = slab_module(policy_source, basis->max_degree, slab->family, mod);
+    CUfunc fn = nullptr;
+    if (err.empty()) err = get_function(mod, "pdg_slab_prepass", fn);
+    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
+    SlabArgs a = slab_args(mesh, basis, rules, params, slab, frames, sigma, face_flow, err_flags);
+    void* args[] = {&a, &sigma, &face_flow};
+    if (api().cuLaunchKernel(fn, (unsigned)grid_for(mesh->n_faces, 128), 1, 1, 128, 1, 1, 0, (cudaStream_t)stream,
+                             args, nullptr) != 0)
+      return fail(PDG_ERR_CUDA, "cuLaunchKernel(pdg_slab_prepass) failed");
+    note_launch();
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+extern "C" int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, const char* policy_source,
+                                 const pdg_rules* rules, const pdg_params* params, const pdg_slab* slab,
+                                 const pdg_pattern* pattern, const pdg_frames* frames, const double* sigma,
+                                 const int8_t* face_flow, double* values, double* rhs, uint32_t* err_flags,
+                                 pdg_stream stream) {
+  PDG_TRY {
+    int rc = slab_check(mesh, basis, policy_source, rules, params, slab);
+    if (rc) return rc;
+    if (!pattern || !frames || !frames->simplex || !frames->facet || !sigma || !face_flow || !values || !rhs)
+      return fail(PDG_ERR_INVALID, "null argument");
+    if (!pattern->nbr_ptr || !pattern->nbr_elem || !pattern->nbr_iface || !pattern->row_len ||
+        !pattern->elem_val_offset)
+      return fail(PDG_ERR_INVALID, "pattern not built (pdg_adjacency / pdg_pattern_offsets)");
+    if (pattern->n_row_elements <= 0) return PDG_OK;
+    const int P = basis->max_degree, fam = slab->family, nw = slab_warps();
+    CUmod mod = nullptr;
+    std::string err = slab_module(policy_source, P, fam, mod);
+    CUfunc fn = nullptr;
+    if (err.empty()) err = get_function(mod, "pdg_slab_kernel", fn);
+    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
+    SlabArgs a = slab_args(mesh, basis, rules, params, slab, frames, sigma, face_flow, err_flags);
+    a.pat = *pattern;
+    a.values = values;
+    a.rhs = rhs;
+    const int nb = slab_nb(P, fam), nt = (nb + 7) / 8;
+    const size_t smem = slab_smem_bytes(slab->table_rows, nt * 8, nt, nw);
+    Api& A = api();
+    if (A.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES_, (int)smem) != 0)
+      return fail(PDG_ERR_CUDA, "cuFuncSetAttribute(max dynamic smem) failed");
+    int per_sm = 0;
+    if (A.cuOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * nw, smem) != 0 || per_sm < 1) per_sm = 1;
+    const int64_t grid = std::min<int64_t>(pattern->n_row_elements, (int64_t)num_sms() * per_sm);
+    void* args[] = {&a};
+    if (A.cuLaunchKernel(fn, (unsigned)grid, 1, 1, 32 * nw, 1, 1, (unsigned)smem, (cudaStream_t)stream, args,
+                         nullptr) != 0)
+      return fail(PDG_ERR_CUDA, "cuLaunchKernel(pdg_slab_kernel) failed");
     note_launch();
     return PDG_OK;
   }

@@ -251,6 +251,19 @@ __device__ __forceinline__ double facet_frame(const pdg_mesh& m, int64_t row, do
   return sqrt(fmax(g, 0.0));
 }
 
+// x = v0 + xi E from a frame record (v0 then E rows), returns the stored measure
+template <int DIM, int K>
+__device__ __forceinline__ double frame_point(const double* fr, const double* xi, double* x) {
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    double acc = fr[i];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc += xi[j] * fr[DIM + j * DIM + i];
+    x[i] = acc;
+  }
+  return fr[DIM + K * DIM];
+}
+
 // ---------------------------------------------------------------------------
 // DMMA m8n8k4 (fp64):  D(8x8) += A(8x4) * B(4x8)
 //   lane = 4*g + t :  a = A[g][t],  b = B[t][g],  c0/c1 = C[g][2t], C[g][2t+1]

@@ -1,0 +1,832 @@
+// Space-time slab kernel: one CTA owns one prism (spatial element x (t0, t1))
+// and produces all of its CSR rows and its RHS segment in a single pass:
+//
+//   volume   sub-prisms (fine spatial triangle x interval), tensor rule
+//            (simplex rule x interval rule of order 2p + quad_increment,
+//            polydg spacetime.py:178-193, quadrature.py:159-178), the
+//            volume terms of assembly.py:396-415 in (x, y, t)
+//   lateral  spatial faces x interval, normal (n, 0) (spacetime.py:265-285):
+//            interior blocks (assembly.py:418-463, both traces evaluated
+//            here, e's rows only), Dirichlet / inflow / Neumann
+//            (assembly.py:466-512) with the lateral tags of SlabGeometry
+//   bottom   the spatial subdivision at t0, statically inflow (normal
+//            (0, 0, -1)): the time jump, with the previous slab's trace or
+//            the initial data as boundary values (spacetime.py:208-227,
+//            355-388); top facets are outflow and contribute nothing.
+//
+// Why a CTA per prism (the spatial kernel uses a warp per element): a PQ
+// basis has (p+1) C(p+2,2) functions -- 18 / 40 / 75 at p = 2 / 3 / 4 -- so
+// one element's row block is up to 10 x 10 DMMA tiles; it is spread over the
+// CTA's warps as a WR x WC grid of tile blocks (fragment reuse: TR + TC
+// shared loads per TR x TC DMMAs), with the k dimension split over WK warp
+// groups when the block is small.  Quadrature points are tabulated 32 per
+// round (lane = point) into a shared table [row][function][slot]; the warps
+// split the functions (a compile-time part per warp, no divergence).
+//
+// Coefficients come in through the runtime-generated policy class CF
+// (model.py policy_source; dim = 3 coordinates, time last) exactly like the
+// spatial kernel: fields inline, kind flags and zero entries compile time.
+#pragma once
+
+#include "sipg_device.cuh"
+
+namespace pdg {
+
+constexpr int SLAB_KS = 32;       // quadrature slots per round (lane = slot)
+constexpr int SLAB_KSP = 36;      // slot stride (4 mod 16 doubles: conflict-free fragment loads)
+constexpr int SLAB_NBR_MAX = 64;  // neighbours per element staged in shared memory
+constexpr int SLAB_NSC = 8;       // per-slot scalar rows
+
+template <int N>
+struct IC {
+  static constexpr int value = N;
+};
+
+// multi-index table of the slab basis (basis.py:86-104): family P = graded
+// lex in (x, y, t); family PQ = spatial graded lex x time degree, time outer.
+template <int P, bool PQ>
+struct SlabMI {
+  static constexpr int NS = binom(P + 2, 2);
+  static constexpr int NB = PQ ? (P + 1) * NS : binom(P + 3, 3);
+  int a[NB][3];
+  __host__ __device__ constexpr SlabMI() : a{} {
+    int f = 0;
+    if (PQ) {
+      for (int k = 0; k <= P; ++k)
+        for (int tot = 0; tot <= P; ++tot)
+          for (int i = 0; i <= tot; ++i) {
+            a[f][0] = i;
+            a[f][1] = tot - i;
+            a[f][2] = k;
+            ++f;
+          }
+    } else {
+      for (int tot = 0; tot <= P; ++tot)
+        for (int i = 0; i <= tot; ++i)
+          for (int j = 0; j <= tot - i; ++j) {
+            a[f][0] = i;
+            a[f][1] = j;
+            a[f][2] = tot - i - j;
+            ++f;
+          }
+    }
+  }
+};
+
+template <int P, bool PQ>
+struct SlabTab {
+  static constexpr int NB = SlabMI<P, PQ>::NB;
+  double v1[3][P + 1], d1[3][P + 1];
+  __device__ __forceinline__ void load(const BoxConst<3>& b, const double* x) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) legendre_1d<P>((x[i] - b.c[i]) * b.ih[i], b.rs[i], b.ih[i], v1[i], d1[i]);
+  }
+  __device__ __forceinline__ double val(int f) const {
+    constexpr SlabMI<P, PQ> mi{};
+    return v1[0][mi.a[f][0]] * v1[1][mi.a[f][1]] * v1[2][mi.a[f][2]];
+  }
+  __device__ __forceinline__ double grad(int f, int k) const {
+    constexpr SlabMI<P, PQ> mi{};
+    if (mi.a[f][k] == 0) return 0.0;
+    return (k == 0 ? d1[0][mi.a[f][0]] : v1[0][mi.a[f][0]]) * (k == 1 ? d1[1][mi.a[f][1]] : v1[1][mi.a[f][1]]) *
+           (k == 2 ? d1[2][mi.a[f][2]] : v1[2][mi.a[f][2]]);
+  }
+};
+
+// warp grid over the row block's 8x8 tiles
+template <int NT, int NW>
+struct SlabTiles {
+  static constexpr int WR = NT <= 3 ? 1 : 2;
+  static constexpr int WC = (NT <= 6 || NW < 4) ? 1 : 2;
+  static constexpr int WK = NW / (WR * WC);
+  static constexpr int TR = (NT + WR - 1) / WR;
+  static constexpr int TC = (NT + WC - 1) / WC;
+};
+
+struct SlabArgs {
+  pdg_mesh m;       // spatial mesh
+  pdg_basis B;      // slab basis: degrees, prism boxes [n][2][3], DoF offsets
+  pdg_rules R;      // spatial triangle rules (vol) + interval rules (face; also the time rules)
+  pdg_params prm;
+  pdg_pattern pat;
+  pdg_slab sl;
+  const double* sframe;  // spatial simplex frames [n_simplices][8], element order
+  const double* fframe;  // spatial facet frames [n_facets][8]
+  const double* sigma;   // lateral penalty per spatial face
+  const int8_t* flow;    // lateral flow side per spatial face
+  double* values;
+  double* rhs;
+  uint32_t* flags;
+};
+
+// shared-memory plan (doubles): table, per-slot scalars, RHS accumulator, neighbour staging
+inline __host__ __device__ int slab_rows(int diff_kind, bool diag, int n_active, bool has_vr, bool has_src) {
+  int vol = diff_kind == PDG_DIFF_NONE ? 0 : (diag ? n_active : 6);
+  vol += has_vr ? 2 : (has_src ? 1 : 0);
+  return vol > 4 ? vol : 4;
+}
+inline __host__ __device__ int slab_table_doubles(int rows, int nbp, int nt, int nw) {
+  const int t = rows * nbp * SLAB_KSP;
+  // split-K reduction buffer aliases the table: (WK-1) * WR*WC * TR*TC * 64
+  const int WR = nt <= 3 ? 1 : 2;
+  const int WC = (nt <= 6 || nw < 4) ? 1 : 2;
+  const int WK = nw / (WR * WC);
+  const int TR = (nt + WR - 1) / WR, TC = (nt + WC - 1) / WC;
+  const int red = (WK - 1) * WR * WC * TR * TC * 64;
+  return t > red ? t : red;
+}
+inline __host__ __device__ size_t slab_smem_bytes(int rows, int nbp, int nt, int nw) {
+  return ((size_t)slab_table_doubles(rows, nbp, nt, nw) + SLAB_NSC * SLAB_KS + nbp) * 8 +
+         (size_t)SLAB_NBR_MAX * 4 * sizeof(int32_t);
+}
+
+template <class CF>
+struct SlabRowsOf {
+  static constexpr bool DIAG = CF::a_diag();
+  __device__ static constexpr int n_active() {
+    return (CF::a_nz(0, 0) ? 1 : 0) + (CF::a_nz(1, 1) ? 1 : 0) + (CF::a_nz(2, 2) ? 1 : 0);
+  }
+  __device__ static constexpr int rowG(int c) {  // table row of the gradient in direction c (diag case)
+    return c == 0 ? 0 : (c == 1 ? (CF::a_nz(0, 0) ? 1 : 0) : (CF::a_nz(0, 0) ? 1 : 0) + (CF::a_nz(1, 1) ? 1 : 0));
+  }
+  __device__ static constexpr int nG() {
+    return CF::diff_kind() == PDG_DIFF_NONE ? 0 : (DIAG ? n_active() : 6);
+  }
+  static constexpr bool HAS_VR = CF::has_adv() || CF::has_reac();
+  __device__ static constexpr int rV() { return nG(); }
+};
+
+// flux n.(A grad phi) with the lateral normal (n_s, 0)
+template <int P, bool PQ, class CF>
+__device__ __forceinline__ double slab_flux(const CF& cf, const SlabTab<P, PQ>& tb, int f, const double* n,
+                                            const double* x) {
+  double fl = 0.0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    double ag = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (CF::a_nz(i, j)) ag += cf.a_ij(i, j, x) * tb.grad(f, j);
+    fl += n[i] * ag;
+  }
+  return fl;
+}
+
+template <int TR, int TC>
+__device__ __forceinline__ void slab_zero(double (&c)[TR][TC][2]) {
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+}
+
+// split-K reduction of the tile accumulators into the wk == 0 warps
+// (all threads of the CTA call it; the buffer aliases the table)
+template <int TR, int TC, int WK, int WRC>
+__device__ __forceinline__ void slab_reduce(double (&c)[TR][TC][2], double* red, int wk, int wrc, int lane) {
+  if (WK == 1) return;
+  __syncthreads();
+  if (wk > 0) {
+    double* o = red + (((wk - 1) * WRC + wrc) * TR * TC) * 64;
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < TC; ++j) {
+        o[((i * TC + j) * 32 + lane) * 2 + 0] = c[i][j][0];
+        o[((i * TC + j) * 32 + lane) * 2 + 1] = c[i][j][1];
+      }
+  }
+  __syncthreads();
+  if (wk == 0) {
+    for (int k = 1; k < WK; ++k) {
+      const double* o = red + (((k - 1) * WRC + wrc) * TR * TC) * 64;
+#pragma unroll
+      for (int i = 0; i < TR; ++i)
+#pragma unroll
+        for (int j = 0; j < TC; ++j) {
+          c[i][j][0] += o[((i * TC + j) * 32 + lane) * 2 + 0];
+          c[i][j][1] += o[((i * TC + j) * 32 + lane) * 2 + 1];
+        }
+    }
+  }
+  __syncthreads();
+}
+
+template <int TR, int TC>
+__device__ __forceinline__ void slab_store(double* values, int64_t voff, int64_t L, int64_t col0, int ne, int nj,
+                                           const double (&c)[TR][TC][2], int wr, int wc, int g, int t) {
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int r = (wr * TR + i) * 8 + g, cc = (wc * TC + j) * 8 + 2 * t + u;
+        if (r < ne && cc < nj) values[voff + (int64_t)r * L + col0 + cc] = c[i][j][u];
+      }
+}
+
+template <int P, bool PQ, int NW, class CF>
+__device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
+  using MI = SlabMI<P, PQ>;
+  using RW = SlabRowsOf<CF>;
+  constexpr int NB = MI::NB, NT = (NB + 7) / 8, NBP = NT * 8;
+  using TL = SlabTiles<NT, NW>;
+  constexpr int WR = TL::WR, WC = TL::WC, WK = TL::WK, TR = TL::TR, TC = TL::TC;
+  constexpr int FPW = (NBP + NW - 1) / NW;  // functions tabulated per warp
+  constexpr int KSP = SLAB_KSP;
+  constexpr int ROWS_V = RW::nG() + (RW::HAS_VR ? 2 : (CF::has_src() ? 1 : 0));
+  constexpr int ROWS = ROWS_V > 4 ? ROWS_V : 4;
+  constexpr int rV = RW::rV();
+  extern __shared__ double smem[];
+  const pdg_mesh& m = a.m;
+  const pdg_basis& B = a.B;
+  const pdg_rules& R = a.R;
+  const pdg_pattern& pat = a.pat;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp % WR, wc = (warp / WR) % WC, wk = warp / (WR * WC);
+  double* T = smem;  // [ROWS][NBP][KSP]
+  double* red = smem;
+  if (ROWS > a.sl.table_rows) {  // host / policy disagreement: refuse rather than overrun
+    if (threadIdx.x == 0 && blockIdx.x == 0) raise_flag(a.flags, PDG_FLAG_STACK);
+    return;
+  }
+  double* sc = smem + slab_table_doubles(a.sl.table_rows, NBP, NT, NW);  // [SLAB_NSC][32]
+  double* rhs_s = sc + SLAB_NSC * SLAB_KS;                     // [NBP]
+  int32_t* nb_j = reinterpret_cast<int32_t*>(rhs_s + NBP);     // [SLAB_NBR_MAX] x 4
+  int32_t* nb_if = nb_j + SLAB_NBR_MAX;
+  int32_t* nb_col = nb_if + SLAB_NBR_MAX;
+  int32_t* nb_n = nb_col + SLAB_NBR_MAX;
+  auto TAB = [&](int row, int f, int slot) -> double& { return T[(row * NBP + f) * KSP + slot]; };
+  double* const s0_ = sc;             // volume: w a_00 (diag) / w (full) | face: alpha
+  double* const s1_ = sc + 32;        // w a_11 | beta
+  double* const s2_ = sc + 64;        // w a_22
+  double* const sw_ = sc + 96;        // w (V x R term)
+  double* const r1_ = sc + 128;       // RHS weight of the V row
+  double* const r2_ = sc + 160;       // RHS weight of the F row
+  const double t0 = a.sl.t0, tau = a.sl.t1 - a.sl.t0;
+  const bool grad_terms = CF::diff_kind() != PDG_DIFF_NONE && a.prm.include_gradient_terms;
+
+  for (int64_t k = blockIdx.x; k < pat.n_row_elements; k += gridDim.x) {
+    const int32_t e = pat.row_elements ? pat.row_elements[k] : (int32_t)k;
+    const int pe = B.degree[e];
+    const int64_t dof_e = B.dof_offset[e];
+    const int ne = (int)(B.dof_offset[e + 1] - dof_e);
+    const BoxConst<3> bx = box_const<3>(B.box + (int64_t)e * 6);
+    const int64_t voff = pat.elem_val_offset[k];
+    const int64_t Lrow = pat.row_len[k];
+    const int64_t q0 = pat.nbr_ptr[e];
+    const int nnb = (int)(pat.nbr_ptr[e + 1] - q0);
+    if (threadIdx.x == 0) {
+      if (nnb > SLAB_NBR_MAX) raise_flag(a.flags, PDG_FLAG_STACK);
+      int col = 0;
+      for (int q = 0; q < min(nnb, SLAB_NBR_MAX); ++q) {
+        const int32_t j = pat.nbr_elem[q0 + q];
+        const int nj = (int)(B.dof_offset[j + 1] - B.dof_offset[j]);
+        nb_j[q] = j;
+        nb_if[q] = pat.nbr_iface[q0 + q];
+        nb_col[q] = col;
+        nb_n[q] = nj;
+        col += nj;
+      }
+    }
+    for (int f = threadIdx.x; f < NBP; f += NW * 32) rhs_s[f] = 0.0;
+    __syncthreads();
+    int colself = 0;
+    for (int q = 0; q < min(nnb, SLAB_NBR_MAX); ++q)
+      if (nb_j[q] == e) colself = nb_col[q];
+
+    double cd[TR][TC][2];
+    slab_zero<TR, TC>(cd);
+
+    // RHS contribution of a round: rhs_s[f] += sum_slot V[f] r1 + F[f] r2 (one owner per f)
+    auto rhs_round = [&](int rowV, int rowF, int nvalid, bool useF) {
+      for (int f = threadIdx.x; f < NB; f += NW * 32) {
+        double s = 0.0;
+        for (int l = 0; l < nvalid; ++l) {
+          s += TAB(rowV, f, l) * r1_[l];
+          if (useF) s += TAB(rowF, f, l) * r2_[l];
+        }
+        rhs_s[f] += s;
+      }
+    };
+
+    // ---------------------------------------------------------------- volume
+    {
+      const int order = 2 * pe + a.prm.quad_increment;
+      const int r0s = R.vol_offset[order], nqs = R.vol_count[order];
+      const int r0t = R.face_offset[order], nqt = R.face_count[order];
+      const int nq = nqs * nqt;
+      const int64_t s0 = m.elem_ptr[e];
+      const int Q = (int)(m.elem_ptr[e + 1] - s0) * nq;
+      for (int base = 0; base < Q; base += SLAB_KS) {
+        const int nvalid = min(SLAB_KS, Q - base);
+        {
+          const int gq = base + min(lane, nvalid - 1);
+          const double valid = lane < nvalid ? 1.0 : 0.0;
+          const int ls = gq / nq;
+          const int rem = gq - ls * nq;
+          const int is = rem / nqt, it = rem - is * nqt;
+          const double* fr = a.sframe + (s0 + ls) * 8;
+          double x[3];
+          const double det = frame_point<2, 2>(fr, R.points + (r0s + is) * 3, x);
+          x[2] = t0 + tau * R.points[(r0t + it) * 3];
+          const double w = (R.weights[r0s + is] * det) * (tau * R.weights[r0t + it]) * valid;
+          SlabTab<P, PQ> tb;
+          tb.load(bx, x);
+          {
+            // this warp's function part (f compile time, the guard warp uniform)
+#pragma unroll
+            for (int f = 0; f < NBP; ++f) {
+              if (f / FPW != warp) continue;
+              if (CF::diff_kind() != PDG_DIFF_NONE) {
+                if (RW::DIAG) {
+#pragma unroll
+                  for (int c = 0; c < 3; ++c)
+                    if (CF::a_nz(c, c)) TAB(RW::rowG(c), f, lane) = f < NB ? tb.grad(f, c) : 0.0;
+                } else {
+#pragma unroll
+                  for (int c = 0; c < 3; ++c) {
+                    double ag = 0.0;
+                    if (f < NB) {
+#pragma unroll
+                      for (int j = 0; j < 3; ++j)
+                        if (CF::a_nz(c, j)) ag += cf.a_ij(c, j, x) * tb.grad(f, j);
+                    }
+                    TAB(c, f, lane) = f < NB ? tb.grad(f, c) : 0.0;
+                    TAB(3 + c, f, lane) = ag;
+                  }
+                }
+              }
+              if (RW::HAS_VR || CF::has_src()) {
+                const double vv = f < NB ? tb.val(f) : 0.0;
+                TAB(rV, f, lane) = vv;
+                if (RW::HAS_VR) {
+                  double rr = 0.0;
+                  if (f < NB) {
+                    if (CF::has_adv()) {
+#pragma unroll
+                      for (int i = 0; i < 3; ++i)
+                        if (CF::b_nz(i)) rr += cf.b_i(i, x) * tb.grad(f, i);
+                    }
+                    if (CF::has_reac()) rr += cf.c(x) * vv;
+                  }
+                  TAB(rV + 1, f, lane) = rr;
+                }
+              }
+            }
+            if (warp == 0) {
+              if (CF::diff_kind() != PDG_DIFF_NONE) {
+                if (RW::DIAG) {
+                  if (CF::a_nz(0, 0)) s0_[lane] = w * cf.a_ij(0, 0, x);
+                  if (CF::a_nz(1, 1)) s1_[lane] = w * cf.a_ij(1, 1, x);
+                  if (CF::a_nz(2, 2)) s2_[lane] = w * cf.a_ij(2, 2, x);
+                } else {
+                  s0_[lane] = w;
+                }
+              }
+              sw_[lane] = w;
+              r1_[lane] = CF::has_src() ? w * cf.f(x) : 0.0;
+            }
+          }
+        }
+        __syncthreads();
+        const int nk = (nvalid + 3) >> 2;
+        for (int kk = wk; kk < nk; kk += WK) {
+          const int q = kk * 4 + t;
+          if (CF::diff_kind() != PDG_DIFF_NONE) {
+            if (RW::DIAG) {
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                if (!CF::a_nz(c, c)) continue;
+                const double s = (c == 0 ? s0_ : (c == 1 ? s1_ : s2_))[q];
+                double lf[TR], rf[TC];
+#pragma unroll
+                for (int i = 0; i < TR; ++i) lf[i] = s * TAB(RW::rowG(c), ((wr * TR + i) % NT) * 8 + g, q);
+#pragma unroll
+                for (int j = 0; j < TC; ++j) rf[j] = TAB(RW::rowG(c), ((wc * TC + j) % NT) * 8 + g, q);
+#pragma unroll
+                for (int i = 0; i < TR; ++i)
+#pragma unroll
+                  for (int j = 0; j < TC; ++j)
+                    if (wr * TR + i < NT && wc * TC + j < NT) dmma(cd[i][j], lf[i], rf[j]);
+              }
+            } else {
+              const double s = s0_[q];
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                double lf[TR], rf[TC];
+#pragma unroll
+                for (int i = 0; i < TR; ++i) lf[i] = s * TAB(c, ((wr * TR + i) % NT) * 8 + g, q);
+#pragma unroll
+                for (int j = 0; j < TC; ++j) rf[j] = TAB(3 + c, ((wc * TC + j) % NT) * 8 + g, q);
+#pragma unroll
+                for (int i = 0; i < TR; ++i)
+#pragma unroll
+                  for (int j = 0; j < TC; ++j)
+                    if (wr * TR + i < NT && wc * TC + j < NT) dmma(cd[i][j], lf[i], rf[j]);
+              }
+            }
+          }
+          if (RW::HAS_VR) {
+            const double s = sw_[q];
+            double lf[TR], rf[TC];
+#pragma unroll
+            for (int i = 0; i < TR; ++i) lf[i] = s * TAB(rV, ((wr * TR + i) % NT) * 8 + g, q);
+#pragma unroll
+            for (int j = 0; j < TC; ++j) rf[j] = TAB(rV + 1, ((wc * TC + j) % NT) * 8 + g, q);
+#pragma unroll
+            for (int i = 0; i < TR; ++i)
+#pragma unroll
+              for (int j = 0; j < TC; ++j)
+                if (wr * TR + i < NT && wc * TC + j < NT) dmma(cd[i][j], lf[i], rf[j]);
+          }
+        }
+        if (CF::has_src()) rhs_round(rV, rV, nvalid, false);
+        __syncthreads();
+      }
+    }
+
+    // ------------------------------------------------------ face-round helpers
+    // Tabulate one lateral / bottom point into rows 0: V_a, 1: F_a (own) and,
+    // for interior faces, 2: -V_b, 3: F_b (neighbour); the warp's function part.
+    auto face_tab = [&](const SlabTab<P, PQ>& ta, const SlabTab<P, PQ>& tn, const double* nrm, const double* x,
+                        bool two, bool useF) {
+#pragma unroll
+      for (int f = 0; f < NBP; ++f) {
+        if (f / FPW != warp) continue;
+        double va = 0.0, fa = 0.0, vb = 0.0, fb = 0.0;
+        if (f < NB) {
+          va = ta.val(f);
+          if (useF) fa = slab_flux<P, PQ>(cf, ta, f, nrm, x);
+          if (two) {
+            vb = -tn.val(f);
+            if (useF) fb = slab_flux<P, PQ>(cf, tn, f, nrm, x);
+          }
+        }
+        TAB(0, f, lane) = va;
+        TAB(1, f, lane) = fa;
+        if (two) {
+          TAB(2, f, lane) = vb;
+          TAB(3, f, lane) = fb;
+        }
+      }
+    };
+    // C_aa += L1 V_a^T + L2 F_a^T, C_ab += L1 (-V_b)^T + L2 F_b^T with
+    // L1 = alpha V_a + beta F_a, L2 = beta V_a (assemble_body.cuh header)
+    auto face_contract = [&](int nvalid, bool two, bool useF, double (&co)[TR][TC][2]) {
+      const int nk = (nvalid + 3) >> 2;
+      for (int kk = wk; kk < nk; kk += WK) {
+        const int q = kk * 4 + t;
+        const double al = s0_[q], be = s1_[q];
+        double l1[TR], l2[TR];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          const int fr_ = ((wr * TR + i) % NT) * 8 + g;
+          const double va = TAB(0, fr_, q);
+          const double fa = useF ? TAB(1, fr_, q) : 0.0;
+          l1[i] = al * va + be * fa;
+          l2[i] = be * va;
+        }
+#pragma unroll
+        for (int j = 0; j < TC; ++j) {
+          const int fc = ((wc * TC + j) % NT) * 8 + g;
+          const double va = TAB(0, fc, q);
+          const double fa = useF ? TAB(1, fc, q) : 0.0;
+          double nvb = 0.0, fb = 0.0;
+          if (two) {
+            nvb = TAB(2, fc, q);
+            fb = useF ? TAB(3, fc, q) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < TR; ++i) {
+            if (wr * TR + i < NT && wc * TC + j < NT) {
+              dmma(cd[i][j], l1[i], va);
+              if (useF) dmma(cd[i][j], l2[i], fa);
+              if (two) {
+                dmma(co[i][j], l1[i], nvb);
+                if (useF) dmma(co[i][j], l2[i], fb);
+              }
+            }
+          }
+        }
+      }
+    };
+
+    // ------------------------------------------------------ lateral interfaces
+    for (int qn = 0; qn < min(nnb, SLAB_NBR_MAX); ++qn) {
+      const int32_t j = nb_j[qn];
+      if (j == e) continue;
+      const int ifc = nb_if[qn];
+      const int pj = B.degree[j];
+      const BoxConst<3> bo = box_const<3>(B.box + (int64_t)j * 6);
+      const int order = 2 * max(pe, pj) + a.prm.quad_increment;
+      const int r0e = R.face_offset[order], nqe = R.face_count[order];
+      const int nqf = nqe * nqe;  // edge rule x time rule of the same order
+      double co[TR][TC][2];
+      slab_zero<TR, TC>(co);
+      for (int64_t fi = m.iface_ptr[ifc]; fi < m.iface_ptr[ifc + 1]; ++fi) {
+        const int32_t f = m.iface_faces[fi];
+        const int side = m.face_owner[f] == e ? 0 : 1;
+        const double sgn = side ? -1.0 : 1.0;
+        const bool down = CF::has_adv() && a.flow[f] == side;
+        const double sig = a.sigma[f];
+        double nrm[3] = {m.face_normal[(int64_t)f * 2], m.face_normal[(int64_t)f * 2 + 1], 0.0};
+        const int64_t row0 = m.face_ptr[f];
+        const int Pf = (int)(m.face_ptr[f + 1] - row0) * nqf;
+        for (int base = 0; base < Pf; base += SLAB_KS) {
+          const int nvalid = min(SLAB_KS, Pf - base);
+          {
+            const int gq = base + min(lane, nvalid - 1);
+            const double valid = lane < nvalid ? 1.0 : 0.0;
+            const int lr = gq / nqf;
+            const int rem = gq - lr * nqf;
+            const int ie = rem / nqe, it = rem - ie * nqe;
+            double x[3];
+            const double jac = frame_point<2, 1>(a.fframe + (row0 + lr) * 8, R.points + (r0e + ie) * 3, x);
+            x[2] = t0 + tau * R.points[(r0e + it) * 3];
+            const double w = (R.weights[r0e + ie] * jac) * (tau * R.weights[r0e + it]) * valid;
+            SlabTab<P, PQ> ta, tn;
+            ta.load(bx, x);
+            tn.load(bo, x);
+            face_tab(ta, tn, nrm, x, true, grad_terms);
+            if (warp == 0) {
+              double wbn = 0.0;
+              if (down) {
+                double bn = 0.0;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                  if (CF::b_nz(i)) bn += cf.b_i(i, x) * nrm[i];
+                wbn = w * bn;
+              }
+              s0_[lane] = w * sig - sgn * wbn;
+              s1_[lane] = grad_terms ? -0.5 * sgn * w : 0.0;
+            }
+          }
+          __syncthreads();
+          face_contract(nvalid, true, grad_terms, co);
+          __syncthreads();
+        }
+      }
+      slab_reduce<TR, TC, WK, WR * WC>(co, red, wk, wr + WR * wc, lane);
+      if (wk == 0) slab_store<TR, TC>(a.values, voff, Lrow, nb_col[qn], ne, nb_n[qn], co, wr, wc, g, t);
+    }
+
+    // ------------------------------------------------- lateral boundary faces
+    for (int64_t bi = m.elem_bface_ptr[e]; bi < m.elem_bface_ptr[e + 1]; ++bi) {
+      const int32_t f = m.elem_bfaces[bi];
+      const int tag = a.sl.lateral_tag[f];
+      if (tag == PDG_TAG_OUTFLOW) continue;
+      if (tag == PDG_TAG_INTERIOR) {
+        if (threadIdx.x == 0) raise_flag(a.flags, PDG_FLAG_UNCLASSIFIED);
+        continue;
+      }
+      if (tag == PDG_TAG_NEUMANN && !CF::has_neu()) continue;
+      if (tag == PDG_TAG_INFLOW && !CF::has_adv()) continue;
+      const bool matrix = tag != PDG_TAG_NEUMANN;
+      const bool useF = tag == PDG_TAG_DIRICHLET && grad_terms;
+      const double sig = a.sigma[f];
+      const bool wi = tag == PDG_TAG_DIRICHLET && CF::has_adv() && a.flow[f] == 1;
+      const int order = 2 * pe + a.prm.quad_increment;
+      const int r0e = R.face_offset[order], nqe = R.face_count[order];
+      const int nqf = nqe * nqe;
+      double nrm[3] = {m.face_normal[(int64_t)f * 2], m.face_normal[(int64_t)f * 2 + 1], 0.0};
+      const int64_t row0 = m.face_ptr[f];
+      const int Pf = (int)(m.face_ptr[f + 1] - row0) * nqf;
+      double dummy[TR][TC][2];
+      for (int base = 0; base < Pf; base += SLAB_KS) {
+        const int nvalid = min(SLAB_KS, Pf - base);
+        {
+          const int gq = base + min(lane, nvalid - 1);
+          const double valid = lane < nvalid ? 1.0 : 0.0;
+          const int lr = gq / nqf;
+          const int rem = gq - lr * nqf;
+          const int ie = rem / nqe, it = rem - ie * nqe;
+          double x[3];
+          const double jac = frame_point<2, 1>(a.fframe + (row0 + lr) * 8, R.points + (r0e + ie) * 3, x);
+          x[2] = t0 + tau * R.points[(r0e + it) * 3];
+          const double w = (R.weights[r0e + ie] * jac) * (tau * R.weights[r0e + it]) * valid;
+          SlabTab<P, PQ> ta;
+          ta.load(bx, x);
+          face_tab(ta, ta, nrm, x, false, useF);
+          if (warp == 0) {
+            double wbn = 0.0;
+            if (CF::has_adv() && (wi || tag == PDG_TAG_INFLOW)) {
+              double bn = 0.0;
+#pragma unroll
+              for (int i = 0; i < 2; ++i)
+                if (CF::b_nz(i)) bn += cf.b_i(i, x) * nrm[i];
+              wbn = w * bn;
+            }
+            double al = 0.0, be = 0.0, r1 = 0.0, r2 = 0.0;
+            if (tag == PDG_TAG_DIRICHLET) {
+              al = w * sig - (wi ? wbn : 0.0);
+              be = useF ? -w : 0.0;
+              const double gv = CF::has_dir() ? cf.gD(x) : 0.0;
+              r1 = gv * al;
+              r2 = gv * be;
+            } else if (tag == PDG_TAG_INFLOW) {
+              al = -wbn;
+              r1 = (CF::has_dir() ? cf.gD(x) : 0.0) * al;
+            } else {
+              r1 = w * cf.gN(x);
+            }
+            s0_[lane] = al;
+            s1_[lane] = be;
+            r1_[lane] = r1;
+            r2_[lane] = r2;
+          }
+        }
+        __syncthreads();
+        if (matrix) face_contract(nvalid, false, useF, dummy);
+        rhs_round(0, 1, nvalid, useF);
+        __syncthreads();
+      }
+    }
+
+    // ----------------------------------------------- bottom facet (time jump)
+    if (CF::has_adv()) {
+      const int order = 2 * pe + a.prm.quad_increment;
+      const int r0s = R.vol_offset[order], nqs = R.vol_count[order];
+      const int64_t s0 = m.elem_ptr[e];
+      const int Q = (int)(m.elem_ptr[e + 1] - s0) * nqs;
+      const bool prev = a.sl.prev_values != nullptr;
+      BoxConst<3> bp = bx;
+      int64_t pdof = 0;
+      if (prev) {
+        bp = box_const<3>(a.sl.prev_box + (int64_t)e * 6);
+        pdof = a.sl.prev_dof_offset[e];
+      }
+      double dummy[TR][TC][2];
+      for (int base = 0; base < Q; base += SLAB_KS) {
+        const int nvalid = min(SLAB_KS, Q - base);
+        {
+          const int gq = base + min(lane, nvalid - 1);
+          const double valid = lane < nvalid ? 1.0 : 0.0;
+          const int ls = gq / nqs;
+          const int is = gq - ls * nqs;
+          double x[3];
+          const double det = frame_point<2, 2>(a.sframe + (s0 + ls) * 8, R.points + (r0s + is) * 3, x);
+          x[2] = t0;
+          const double w = R.weights[r0s + is] * det * valid;
+          SlabTab<P, PQ> ta;
+          ta.load(bx, x);
+          const double nrm[3] = {0.0, 0.0, 0.0};
+          face_tab(ta, ta, nrm, x, false, false);
+          if (warp == 0) {
+            // b.n with n = (0, 0, -1)
+            const double wbn = CF::b_nz(2) ? -w * cf.b_i(2, x) : 0.0;
+            double gv;
+            if (prev) {
+              SlabTab<P, PQ> tp;
+              tp.load(bp, x);
+              gv = 0.0;
+              const int np_ = (int)(a.sl.prev_dof_offset[e + 1] - pdof);
+#pragma unroll
+              for (int f = 0; f < NB; ++f)
+                if (f < np_) gv += a.sl.prev_values[pdof + f] * tp.val(f);
+            } else {
+              gv = CF::has_u0() ? cf.u0(x) : 0.0;
+            }
+            s0_[lane] = -wbn;
+            s1_[lane] = 0.0;
+            r1_[lane] = -wbn * gv;
+          }
+        }
+        __syncthreads();
+        face_contract(nvalid, false, false, dummy);
+        rhs_round(0, 0, nvalid, false);
+        __syncthreads();
+      }
+    }
+
+    // ------------------------------------------------------------- write-out
+    slab_reduce<TR, TC, WK, WR * WC>(cd, red, wk, wr + WR * wc, lane);
+    if (wk == 0) slab_store<TR, TC>(a.values, voff, Lrow, colself, ne, ne, cd, wr, wc, g, t);
+    for (int f = threadIdx.x; f < ne; f += NW * 32) a.rhs[dof_e + f] = rhs_s[f];
+    // col_idx of all rows (assembly.py:319-324): every row repeats the
+    // concatenated DoF ranges of the sorted neighbours
+    if (a.pat.col_idx) {
+      for (int p = threadIdx.x; p < (int)Lrow; p += NW * 32) {
+        int q = 0;
+        while (q + 1 < min(nnb, SLAB_NBR_MAX) && nb_col[q + 1] <= p) ++q;
+        const int64_t cv = B.dof_offset[nb_j[q]] + (p - nb_col[q]);
+        int64_t* dst = a.pat.col_idx + voff + p;
+        for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Lateral face pre-pass (one thread per spatial face): penalty with the
+// slab's side data (spacetime.py:301-351: a_bar over the prism's volume
+// points with the lateral normal, extruded-split adjacent volumes
+// |K| tau / (s+1), prism volume |k| tau, face measure |F| tau, cap p^(2(d-1))
+// with d = 3) and the flow side over the order-2 lateral sample points
+// (spacetime.py:248-263, 287-309).
+template <class CF>
+__device__ __forceinline__ void slab_prepass_body(const SlabArgs& a, const CF& cf, double* sigma, int8_t* flow) {
+  const pdg_mesh& m = a.m;
+  const pdg_basis& B = a.B;
+  const pdg_rules& R = a.R;
+  const double t0 = a.sl.t0, tau = a.sl.t1 - a.sl.t0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < m.n_faces; f += stride) {
+    const int32_t o = m.face_owner[f], nb = m.face_neighbor[f];
+    const bool interior = nb >= 0;
+    const int tag = interior ? PDG_TAG_INTERIOR : a.sl.lateral_tag[f];
+    const double n[3] = {m.face_normal[f * 2], m.face_normal[f * 2 + 1], 0.0};
+    sigma[f] = 0.0;
+    flow[f] = interior ? -1 : 0;
+    if (!interior && tag != PDG_TAG_DIRICHLET) continue;
+    if (CF::has_adv()) {
+      const int r0 = R.face_offset[2], nq = R.face_count[2];
+      double sum = 0.0, mn = PDG_INF, mx = -PDG_INF, amax = 0.0;
+      int cnt = 0;
+      for (int64_t row = m.face_ptr[f]; row < m.face_ptr[f + 1]; ++row) {
+        const double* fr = a.fframe + row * 8;
+        for (int i = 0; i < nq; ++i)
+          for (int it = 0; it < nq; ++it) {
+            double x[3];
+            frame_point<2, 1>(fr, R.points + (r0 + i) * 3, x);
+            x[2] = t0 + tau * R.points[(r0 + it) * 3];
+            double bn = 0.0;
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              if (CF::b_nz(k)) bn += cf.b_i(k, x) * n[k];
+            sum += bn;
+            mn = fmin(mn, bn);
+            mx = fmax(mx, bn);
+            amax = fmax(amax, fabs(bn));
+            ++cnt;
+          }
+      }
+      const double tol = 1e-10 * fmax(1.0, amax);
+      if (mn < -tol && mx > tol) raise_flag(a.flags, PDG_FLAG_STRADDLE);
+      const double mean = sum / cnt;
+      if (interior) flow[f] = mean < 0.0 ? 0 : (mean > 0.0 ? 1 : -1);
+      else flow[f] = mean < 0.0 ? 1 : 0;
+    }
+    double best = 0.0;
+    for (int side = 0; side < (interior ? 2 : 1); ++side) {
+      const int32_t el = side == 0 ? o : nb;
+      double mxv = -1.0;
+      bool any = false;
+      for (int64_t row = m.face_ptr[f]; row < m.face_ptr[f + 1]; ++row) {
+        const int32_t s = side == 0 ? m.facet_owner_simplex[row] : m.facet_neighbor_simplex[row];
+        if (s < 0) continue;
+        const double v = m.simplex_volumes[s];
+        mxv = any ? fmax(mxv, v) : v;
+        any = true;
+      }
+      if (!any || !(mxv > 0.0)) {
+        raise_flag(a.flags, PDG_FLAG_NO_ADJACENT_SIMPLEX);
+        continue;
+      }
+      const double max_adj = mxv * tau / 3.0;
+      const int p = B.degree[el];
+      const double vol = m.elem_volumes[el] * tau;
+      double cap = PDG_INF;
+      if (a.prm.coverable && a.prm.coverable[el]) cap = (double)p * p * p * p;
+      double ab = 0.0;
+      if (CF::diff_kind() != PDG_DIFF_NONE) {
+        auto nAn = [&](const double* x) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            double r = 0.0;
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              if (CF::a_nz(i, j)) r += cf.a_ij(i, j, x) * n[j];
+            s += n[i] * r;
+          }
+          return s;
+        };
+        if (CF::a_const()) {
+          const double x0[3] = {0.0, 0.0, 0.0};
+          ab = nAn(x0);
+        } else {
+          const int order = 2 * p + a.prm.quad_increment;
+          const int r0s = R.vol_offset[order], nqs = R.vol_count[order];
+          const int r0t = R.face_offset[order], nqt = R.face_count[order];
+          ab = -PDG_INF;
+          for (int64_t si = m.elem_ptr[el]; si < m.elem_ptr[el + 1]; ++si)
+            for (int is = 0; is < nqs; ++is)
+              for (int it = 0; it < nqt; ++it) {
+                double x[3];
+                frame_point<2, 2>(a.sframe + si * 8, R.points + (r0s + is) * 3, x);
+                x[2] = t0 + tau * R.points[(r0t + it) * 3];
+                ab = fmax(ab, nAn(x));
+              }
+        }
+      }
+      const double ratio = fmin(vol / max_adj, cap);
+      best = fmax(best, ratio * ab * (double)(p * p) * (m.face_measure[f] * tau) / vol);
+    }
+    sigma[f] = a.prm.penalty_constant * best;
+  }
+}
+
+}  // namespace pdg

@@ -505,10 +505,31 @@ def cuda_expr(e: Expr) -> str:
     return f"{_CFN[e.op]}({cuda_expr(e.args[0])})"
 
 
-def policy_source(coeffs, dim: int) -> str:
+def policy_source(coeffs, dim: int, initial=None) -> str:
     """CUDA source of the coefficient policy class ``JitCoef`` consumed by
     ``assemble_body`` (csrc/assemble_body.cuh, see InterpCoef for the
-    interface)."""
+    interface) and ``slab_body`` (csrc/slab_body.cuh: additionally the
+    compile-time zero pattern of A and b, and the slab's initial data
+    ``u0`` of the spatial coordinates)."""
+    return _policy(coeffs, dim, initial)[0]
+
+
+def slab_policy(coeffs, initial=None):
+    """(policy source, shared-memory table rows) of a space-time slab
+    (coordinates (x, y, t)); the rows follow ``slab_rows`` in slab_body.cuh."""
+    src, info = _policy(coeffs, 3, initial)
+    kind, diag, n_act = info["kind"], info["diag"], info["n_active"]
+    vol = 0 if kind == 0 else (n_act if diag else 6)
+    has_vr = info["adv"] or info["reac"]
+    vol += 2 if has_vr else (1 if info["src"] else 0)
+    return src, max(vol, 4)
+
+
+def _is_zero(e) -> bool:
+    return e is not None and e.is_constant and float(e.value) == 0.0
+
+
+def _policy(coeffs, dim: int, initial=None):
     ten = as_tensor(coeffs.diffusion, dim, "diffusion")
     kind, ent = 0, None
     if ten is not None:
@@ -521,19 +542,42 @@ def policy_source(coeffs, dim: int) -> str:
     adv = as_vector_exprs(coeffs.advection, dim, "advection")
     sc = {n: as_scalar_expr(getattr(coeffs, f), f) for n, f in
           (("c", "reaction"), ("f", "source"), ("gD", "dirichlet_data"), ("gN", "neumann_data"))}
+    u0 = as_scalar_expr(initial, "initial data") if initial is not None else None
     b = lambda v: "true" if v else "false"
+    # zero pattern of A (entry identically 0) and b
+    if kind == 0:
+        nz = [[False] * dim for _ in range(dim)]
+    elif kind == 1:
+        nz = [[i == j and not _is_zero(ent) for j in range(dim)] for i in range(dim)]
+    else:
+        nz = [[not _is_zero(ent[i * dim + j]) for j in range(dim)] for i in range(dim)]
+    diag = all(not nz[i][j] for i in range(dim) for j in range(dim) if i != j)
+    a_const = kind == 0 or (ent.is_constant if kind == 1 else all(e.is_constant for e in ent))
+    bnz = [adv is not None and not _is_zero(c) for c in (adv or [None] * dim)]
     out = ["struct JitCoef {",
            f"  __device__ static constexpr int diff_kind() {{ return {kind}; }}",
            f"  __device__ static constexpr bool has_adv() {{ return {b(adv is not None)}; }}",
            f"  __device__ static constexpr bool has_reac() {{ return {b(sc['c'] is not None)}; }}",
            f"  __device__ static constexpr bool has_src() {{ return {b(sc['f'] is not None)}; }}",
            f"  __device__ static constexpr bool has_dir() {{ return {b(sc['gD'] is not None)}; }}",
-           f"  __device__ static constexpr bool has_neu() {{ return {b(sc['gN'] is not None)}; }}"]
+           f"  __device__ static constexpr bool has_neu() {{ return {b(sc['gN'] is not None)}; }}",
+           f"  __device__ static constexpr bool has_u0() {{ return {b(u0 is not None)}; }}",
+           f"  __device__ static constexpr bool a_diag() {{ return {b(diag)}; }}",
+           f"  __device__ static constexpr bool a_const() {{ return {b(a_const)}; }}"]
+    nzc = " ".join(f"case {i * dim + j}: return true;" for i in range(dim) for j in range(dim)
+                   if nz[i][j])
+    out.append(f"  __device__ static constexpr bool a_nz(int i, int j) "
+               f"{{ switch (i * {dim} + j) {{ {nzc} default: break; }} return false; }}")
+    bzc = " ".join(f"case {i}: return true;" for i in range(dim) if bnz[i])
+    out.append(f"  __device__ static constexpr bool b_nz(int i) "
+               f"{{ switch (i) {{ {bzc} default: break; }} return false; }}")
     iso = cuda_expr(ent) if kind == 1 else "1.0"
     out.append(f"  __device__ double a_iso(const double* x) const {{ return {iso}; }}")
     cases = ""
     if kind == 2:
         cases = " ".join(f"case {k}: return {cuda_expr(e)};" for k, e in enumerate(ent))
+    elif kind == 1:  # the slab kernel reads A entrywise
+        cases = " ".join(f"case {i * dim + i}: return {iso};" for i in range(dim))
     out.append(f"  __device__ double a_ij(int i, int j, const double* x) const "
                f"{{ switch (i * {dim} + j) {{ {cases} default: break; }} return 0.0; }}")
     cases = ""
@@ -544,8 +588,12 @@ def policy_source(coeffs, dim: int) -> str:
     for n in ("c", "f", "gD", "gN"):
         body = cuda_expr(sc[n]) if sc[n] is not None else "0.0"
         out.append(f"  __device__ double {n}(const double* x) const {{ return {body}; }}")
+    out.append(f"  __device__ double u0(const double* x) const "
+               f"{{ return {cuda_expr(u0) if u0 is not None else '0.0'}; }}")
     out.append("};")
-    return "\n".join(out)
+    info = dict(kind=kind, diag=diag, n_active=sum(nz[i][i] for i in range(dim)),
+                adv=adv is not None, reac=sc["c"] is not None, src=sc["f"] is not None)
+    return "\n".join(out), info
 
 
 def _pi_multiple(v: float):

@@ -120,3 +120,416 @@ def load_solution_vector(path) -> np.ndarray:
     if data.shape[0] != n:
         raise MeshError(f"{path}: truncated solution vector")
     return data.astype(float)
+
+
+# -- lateral boundary classification (host pre-pass) ---------------------------------
+
+def classify_lateral_faces(flat, t0, t1, coeffs, dirichlet_predicate=None) -> np.ndarray:
+    """Tags of the lateral faces of a slab (``SlabGeometry._classify_lateral``,
+    spacetime.py:229-246), vectorised over the spatial boundary faces: the
+    order-2 facet rule x order-2 interval rule sample points; Dirichlet
+    (or Neumann by predicate) where n^T A n > 1e-12 max(1, |A|) at their mean,
+    else inflow / outflow by the sign of the mean b.n.  Interior faces get 0.
+    polydg classifies inside the geometry constructor, i.e. per assembly, on
+    the host; so does this (boundary faces only, a few per cent of faces)."""
+    from .model import _checked_flow_sign_grouped, _face_sample_points
+    from .mesh import BOUNDARY, BoundaryTag, tag_code
+    from .quadrature import interval_rule
+
+    tags = np.zeros(flat.n_faces, np.int8)
+    bf = np.flatnonzero(flat.face_neighbor == BOUNDARY)
+    if bf.size == 0:
+        return tags
+    sp, which, counts = _face_sample_points(flat, bf)
+    tr = interval_rule(2)
+    tau = t1 - t0
+    tp = t0 + tau * tr.points[:, 0]
+    nt = tp.shape[0]
+    pts = np.empty((sp.shape[0] * nt, 3))
+    pts[:, :2] = np.repeat(sp, nt, axis=0)
+    pts[:, 2] = np.tile(tp, sp.shape[0])
+    which = np.repeat(which, nt)
+    counts = counts * nt
+    n3 = np.zeros((bf.size, 3))
+    n3[:, :2] = flat.face_normal[bf]
+    mean = np.add.reduceat(pts, np.r_[0, np.cumsum(counts)[:-1]], axis=0) / counts[:, None]
+    out = np.full(bf.size, tag_code(BoundaryTag.OUTFLOW), np.int8)
+    decided = np.zeros(bf.size, bool)
+    if coeffs.diffusion is not None:
+        a = np.asarray(coeffs.diffusion(mean))
+        tol = 1e-12 * np.maximum(1.0, np.abs(a).reshape(bf.size, -1).max(axis=1))
+        ell = np.einsum("fi,fij,fj->f", n3, a, n3) > tol
+        dirich = ell.copy()
+        if dirichlet_predicate is not None:
+            for k in np.flatnonzero(ell):
+                dirich[k] = bool(dirichlet_predicate(mean[k]))
+        out[ell & dirich] = tag_code(BoundaryTag.DIRICHLET)
+        out[ell & ~dirich] = tag_code(BoundaryTag.NEUMANN)
+        decided |= ell
+    if coeffs.advection is not None:
+        rest = ~decided
+        bn = np.einsum("qd,qd->q", np.asarray(coeffs.advection(pts)), n3[which])
+        sign = _checked_flow_sign_grouped(bn, counts, "a lateral slab face", rest)
+        out[rest & (sign < 0.0)] = tag_code(BoundaryTag.INFLOW)
+    tags[bf] = out
+    return tags
+
+
+# -- the device plan ------------------------------------------------------------------
+
+class SlabPlan:
+    """Device buffers + descriptors for repeated assembly of one slab.
+
+    ``run()`` enqueues, on one stream and without host synchronisation: the
+    index phase (adjacency, row offsets -- shared with the spatial engine, on
+    the prism DoF map), the spatial affine frames, the lateral face pre-pass
+    (sigma, flow side) and the fused slab kernel (values + col_idx + RHS).
+    """
+
+    def __init__(self, slab, coeffs, specs, u_prev, config=None, row_elements=None, device=None,
+                 stream=None, dirichlet_predicate=None):
+        import ctypes as C
+
+        from . import _lib
+        from .assembly import AssemblyConfig, AssemblyError, DeviceRules, DofMap, _torch, device_mesh
+        from .basis import num_basis, spec_arrays
+        from .model import as_scalar_expr, slab_policy
+
+        torch = _torch()
+        self.lib = _lib.load()
+        config = config or AssemblyConfig()
+        self.config = config
+        self.slab = slab
+        self.dm = device_mesh(slab.spatial, device)
+        dev = self.device = self.dm.device
+        flat = self.flat = self.dm.flat
+        if flat.dim != 2:
+            raise NotImplementedError("the device slab engine supports 2D spatial meshes (3D prisms)")
+        deg, boxes, fam = spec_arrays(specs)
+        fname = family_name(fam)
+        if deg.shape[0] != flat.n_elements:
+            raise AssemblyError("one BasisSpec per element required")
+        if boxes.shape[1:] != (2, 3):
+            raise ValueError("slab spec boxes must be (2, 3): spatial box x interval")
+        pmax = int(deg.max()) if deg.size else 0
+        if pmax > _lib.SLAB_MAX_DEGREE:
+            raise NotImplementedError(f"slab degree {pmax} exceeds the device range (p <= {_lib.SLAB_MAX_DEGREE})")
+        if fname == "PQ" and np.any(deg != pmax):
+            raise NotImplementedError("family PQ slabs need a uniform degree on the device")
+        counts = np.array([num_basis(int(p), 3, fam) for p in deg], np.int64)
+        self.dof = DofMap(np.concatenate([[0], np.cumsum(counts)]).astype(np.int64))
+        self.degrees = deg
+        inc = int(config.quad_increment)
+        pen = config.penalty
+        self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        self.t = {"degree": T(deg.astype(np.int32)), "box": T(boxes), "dof": T(self.dof.offsets),
+                  "sbox": T(np.ascontiguousarray(boxes[:, :, :2]))}
+        b = _lib.Basis()
+        b.max_degree = pmax
+        b.degree, b.box, b.dof_offset = _lib.ptr(self.t["degree"]), _lib.ptr(self.t["box"]), _lib.ptr(self.t["dof"])
+        self.basis = b
+        sb = _lib.Basis()  # spatial view for the frame pre-pass (2D boxes)
+        sb.max_degree = pmax
+        sb.degree, sb.box, sb.dof_offset = b.degree, _lib.ptr(self.t["sbox"]), b.dof_offset
+        self.sbasis = sb
+
+        uniq = np.unique(deg)
+        vol_orders = [2 * int(p) + inc for p in uniq]
+        face_orders = [2 * int(max(p, q)) + inc for p in uniq for q in uniq] + vol_orders
+        self.rules = DeviceRules(2, vol_orders, face_orders, dev)
+
+        # time-jump data (spacetime.py:367-388)
+        initial = None
+        self.t["prev"] = self.t["prev_dof"] = self.t["prev_box"] = None
+        if u_prev is None:
+            raise MeshError("slab assembly needs initial data or a previous solution")
+        if callable(u_prev) and not isinstance(u_prev, tuple):
+            initial = as_scalar_expr(u_prev, "initial data")
+        else:
+            pspecs, pvec = u_prev
+            pdeg, pbox, pfam = spec_arrays(pspecs)
+            pvec = np.asarray(pvec, dtype=np.float64)
+            pcounts = np.array([num_basis(int(p), 3, pfam) for p in pdeg], np.int64)
+            if pcounts.sum() != pvec.shape[0]:
+                raise MeshError(f"previous solution has {pvec.shape[0]} dofs, expected {int(pcounts.sum())}")
+            if pdeg.shape[0] != flat.n_elements:
+                raise MeshError("previous slab has a different spatial element count")
+            if family_name(pfam) != fname or np.any(pdeg != deg):
+                raise NotImplementedError("the device time jump needs the previous slab's degree and family")
+            self.t["prev"] = T(pvec)
+            self.t["prev_dof"] = T(np.concatenate([[0], np.cumsum(pcounts)]).astype(np.int64))
+            self.t["prev_box"] = T(pbox)
+        self.policy, rows = slab_policy(coeffs, initial)
+        self.policy = self.policy.encode()
+        _lib.check(self.lib.pdg_slab_prepare(self.policy, pmax, 1 if fname == "PQ" else 0))
+
+        tags = classify_lateral_faces(flat, slab.t0, slab.t1, coeffs, dirichlet_predicate)
+        self.lateral_tags = tags
+        self.t["lat"] = T(tags if tags.size else np.zeros(1, np.int8))
+        s = _lib.Slab()
+        s.t0, s.t1 = float(slab.t0), float(slab.t1)
+        s.lateral_tag = _lib.ptr(self.t["lat"])
+        s.prev_values = _lib.ptr(self.t["prev"])
+        s.prev_dof_offset = _lib.ptr(self.t["prev_dof"])
+        s.prev_box = _lib.ptr(self.t["prev_box"])
+        s.family = 1 if fname == "PQ" else 0
+        s.table_rows = rows
+        self.sdesc = s
+
+        prm = _lib.Params()
+        prm.quad_increment = inc
+        prm.include_gradient_terms = 1
+        prm.penalty_constant = float(pen.constant)
+        if pen.coverable is not None:
+            self.t["coverable"] = T(np.asarray(pen.coverable, bool).astype(np.uint8))
+            prm.coverable = _lib.ptr(self.t["coverable"])
+        self.params = prm
+
+        nel = flat.n_elements
+        if row_elements is None:
+            self.row_elements = np.arange(nel, dtype=np.int64)
+            self.t["rows"] = None
+        else:
+            self.row_elements = np.unique(np.asarray(row_elements, dtype=np.int64))
+            self.t["rows"] = T(self.row_elements.astype(np.int32))
+        nr = self.row_elements.shape[0]
+        self.n_local_rows = int(counts[self.row_elements].sum())
+        z = lambda n, dt: torch.empty(max(int(n), 1), dtype=dt, device=dev)
+        i64, i32 = torch.int64, torch.int32
+        nadj = nel + 2 * flat.n_interfaces
+        self.t.update(nbr_ptr=z(nel + 1, i64), nbr_elem=z(nadj, i32), nbr_iface=z(nadj, i32),
+                      row_len=z(nr, i64), val_off=z(nr + 1, i64), row_off=z(nr + 1, i64),
+                      row_ptr=z(self.n_local_rows + 1, i64),
+                      sigma=z(flat.n_faces, torch.float64), flow=z(flat.n_faces, torch.int8),
+                      flags=torch.zeros(1, dtype=torch.int32, device=dev),
+                      sframe=z(flat.n_simplices * 8, torch.float64), fframe=z(flat.n_facets * 8, torch.float64),
+                      erec=z(nel * 8, torch.float64))
+        fr = _lib.Frames()
+        fr.simplex, fr.facet, fr.element = _lib.ptr(self.t["sframe"]), _lib.ptr(self.t["fframe"]), _lib.ptr(self.t["erec"])
+        self.frames = fr
+        self.ws_bytes = int(self.lib.pdg_workspace_bytes(nel, flat.n_interfaces))
+        self.t["ws"] = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        pat = _lib.Pattern()
+        pat.n_row_elements = nr
+        pat.row_elements = _lib.ptr(self.t["rows"])
+        pat.nbr_ptr, pat.nbr_elem, pat.nbr_iface = (_lib.ptr(self.t["nbr_ptr"]), _lib.ptr(self.t["nbr_elem"]),
+                                                    _lib.ptr(self.t["nbr_iface"]))
+        pat.row_len, pat.elem_val_offset, pat.elem_row_offset = (
+            _lib.ptr(self.t["row_len"]), _lib.ptr(self.t["val_off"]), _lib.ptr(self.t["row_off"]))
+        pat.row_ptr = _lib.ptr(self.t["row_ptr"])
+        self.pattern = pat
+        with torch.cuda.stream(self.stream):
+            self._index_phase(size_query=True)
+        self.t["col_idx"] = z(self.nnz, i64)
+        self.t["values"] = z(self.nnz, torch.float64)
+        self.t["rhs"] = torch.zeros(max(self.dof.n_dofs, 1), dtype=torch.float64, device=dev)
+        pat.col_idx = _lib.ptr(self.t["col_idx"])
+        self._C = C
+
+    def _index_phase(self, size_query=False):
+        from . import _lib
+
+        C = __import__("ctypes")
+        s = _lib.stream_ptr(self.stream)
+        _lib.check(self.lib.pdg_adjacency(C.byref(self.dm.struct), _lib.ptr(self.t["nbr_ptr"]),
+                                          _lib.ptr(self.t["nbr_elem"]), _lib.ptr(self.t["nbr_iface"]),
+                                          _lib.ptr(self.t["ws"]), self.ws_bytes, s))
+        nnz = C.c_int64(0)
+        _lib.check(self.lib.pdg_pattern_offsets(C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.pattern),
+                                                self.n_local_rows, C.byref(nnz) if size_query else None,
+                                                _lib.ptr(self.t["ws"]), self.ws_bytes, s))
+        if size_query:
+            self.nnz = int(nnz.value)
+
+    def _prepass(self):
+        from . import _lib
+
+        C = self._C
+        s = _lib.stream_ptr(self.stream)
+        _lib.check(self.lib.pdg_frames_build(C.byref(self.dm.struct), C.byref(self.sbasis), C.byref(self.frames),
+                                             _lib.ptr(self.t["flags"]), s))
+        _lib.check(self.lib.pdg_slab_prepass(
+            C.byref(self.dm.struct), C.byref(self.basis), self.policy, C.byref(self.rules.struct),
+            C.byref(self.params), C.byref(self.sdesc), C.byref(self.frames), _lib.ptr(self.t["sigma"]),
+            _lib.ptr(self.t["flow"]), _lib.ptr(self.t["flags"]), s))
+
+    def _elements(self):
+        from . import _lib
+
+        C = self._C
+        _lib.check(self.lib.pdg_slab_assemble(
+            C.byref(self.dm.struct), C.byref(self.basis), self.policy, C.byref(self.rules.struct),
+            C.byref(self.params), C.byref(self.sdesc), C.byref(self.pattern), C.byref(self.frames),
+            _lib.ptr(self.t["sigma"]), _lib.ptr(self.t["flow"]), _lib.ptr(self.t["values"]),
+            _lib.ptr(self.t["rhs"]), _lib.ptr(self.t["flags"]), _lib.stream_ptr(self.stream)))
+
+    def run(self, events=None):
+        """Enqueue index phase + pre-pass + slab kernel; no host sync."""
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            if events:
+                events[0].record(self.stream)
+            self._index_phase()
+            if events:
+                events[1].record(self.stream)
+            self._prepass()
+            if events:
+                events[2].record(self.stream)
+            self._elements()
+            if events:
+                events[3].record(self.stream)
+
+    def check_flags(self):
+        from . import _lib
+        from .assembly import _raise_flags
+
+        self.stream.synchronize()
+        flags = int(self.t["flags"].item())
+        if flags & _lib.FLAG_STACK:
+            raise NotImplementedError("slab element with more than 64 neighbours (device staging capacity)")
+        _raise_flags(flags)
+
+    # -- results ----------------------------------------------------------------
+    @property
+    def values(self):
+        return self.t["values"][: self.nnz]
+
+    @property
+    def col_idx(self):
+        return self.t["col_idx"][: self.nnz]
+
+    @property
+    def row_ptr(self):
+        return self.t["row_ptr"][: self.n_local_rows + 1]
+
+    @property
+    def rhs(self):
+        return self.t["rhs"][: self.dof.n_dofs]
+
+    def to_csr(self):
+        from .assembly import CSRMatrix
+
+        return CSRMatrix(self.n_local_rows, self.dof.n_dofs, self.row_ptr.cpu().numpy(),
+                         self.col_idx.cpu().numpy(), self.values.cpu().numpy())
+
+    def work_stats(self):
+        """polydg per-kernel work items (assembly.py:360-391) of the slab: volume
+        items = sub-prisms, interior = lateral sub-facets, inflow includes the
+        bottom facets (one per sub-prism), top facets are outflow items."""
+        from .assembly import KERNEL_NAMES, KernelTiming
+        from .mesh import BOUNDARY, TAG_CODE
+
+        f = self.flat
+        counts = np.diff(self.dof.offsets)
+        owned = np.zeros(f.n_elements, bool)
+        owned[self.row_elements] = True
+        nsim = np.diff(f.elem_ptr)
+        out = {k: KernelTiming(k) for k in KERNEL_NAMES}
+        out["element"].work_items = int(nsim[owned].sum())
+        out["element"].nnz_written = int((nsim * counts * counts)[owned].sum())
+        nfac = np.diff(f.face_ptr)
+        o, nb = f.face_owner, f.face_neighbor
+        inter = nb != BOUNDARY
+        oo = owned[o]
+        on = np.where(inter, owned[np.where(inter, nb, 0)], False)
+        no, nn = counts[o], counts[np.where(inter, nb, 0)]
+        per = np.where(oo & on, (no + nn) ** 2, np.where(oo, no * (no + nn), nn * (no + nn)))
+        sel = inter & (oo | on)
+        out["interior"].work_items = int(nfac[sel].sum())
+        out["interior"].nnz_written = int((per * nfac)[sel].sum())
+        tg = self.lateral_tags
+        for name, codes in (("dirichlet", (TAG_CODE["dirichlet"],)), ("inflow", (TAG_CODE["inflow"],)),
+                            ("neumann_outflow", (TAG_CODE["neumann"], TAG_CODE["outflow"]))):
+            m = (~inter) & oo & np.isin(tg, codes)
+            out[name].work_items = int(nfac[m].sum())
+            if name != "neumann_outflow":
+                out[name].nnz_written = int((nfac * no * no)[m].sum())
+        out["inflow"].work_items += int(nsim[owned].sum())
+        out["inflow"].nnz_written += int((nsim * counts * counts)[owned].sum())
+        out["neumann_outflow"].work_items += int(nsim[owned].sum())
+        return out
+
+
+@dataclass
+class ParabolicProblem:
+    """Space-time description of a parabolic model problem (polydg
+    model.py:263-275): block-form fields in (x, y, t) (diffusion
+    [[a, 0], [0, 0]], advection (w, 1)) and initial data of the spatial
+    coordinates."""
+
+    spatial_dim: int
+    coeffs: object
+    initial: object
+    t_final: float = 1.0
+
+
+def assemble_slab(slab, coeffs, specs, u_prev, config=None, approach=2, dirichlet_predicate=None,
+                  row_elements=None):
+    """Assemble one slab system on the B200 (polydg ``spacetime.assemble_slab``,
+    spacetime.py:391-413).  ``u_prev``: initial-data field of the spatial
+    points (an Expr / ScalarField: it is evaluated on the device) for the
+    first slab, or ``(previous specs, previous coefficient vector)``.
+    ``approach`` 1 and 2 run the same preset-sparsity engine (polydg's two
+    approaches agree within 1e-12).  Returns (CSRMatrix, rhs, AssemblyStats)."""
+    import time
+
+    import torch
+
+    from .assembly import AssemblyStats
+
+    if approach not in (1, 2):
+        raise ValueError("approach must be 1 or 2")
+    t_start = time.perf_counter()
+    plan = SlabPlan(slab, coeffs, specs, u_prev, config, row_elements=row_elements,
+                    dirichlet_predicate=dirichlet_predicate)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    plan.run(ev)
+    plan.check_flags()
+    ms_index, ms_pre, ms_el = (ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]))
+    kern = plan.work_stats()
+    kern["element"].seconds = ms_el * 1e-3
+    kern["interior"].seconds = ms_pre * 1e-3
+    stats = AssemblyStats(kernels=kern, index_seconds=ms_index * 1e-3, kernel_wall_seconds=(ms_pre + ms_el) * 1e-3,
+                          triplet_count=sum(k.nnz_written for k in kern.values()), nnz=plan.nnz,
+                          device_ms={"index": ms_index, "prepass": ms_pre, "element": ms_el})
+    matrix = plan.to_csr()
+    rhs = plan.rhs.cpu().numpy().copy()
+    stats.total_seconds = time.perf_counter() - t_start
+    return matrix, rhs, stats
+
+
+def _default_solver(matrix, rhs, dof_map):
+    """Sparse direct solve on the host (polydg's default is block-Jacobi GMRES,
+    solver.py:74-118 -- a consumer of the assembly, out of this engine's scope)."""
+    from scipy.sparse.linalg import spsolve
+
+    return spsolve(matrix.to_scipy().tocsc(), rhs)
+
+
+def march(spatial_mesh, time_partition, problem, degrees, family=Family.PQ, config=None, solver=None,
+          approach=2, dirichlet_predicate=None, dump_path=None):
+    """Sequential slab-by-slab solve (polydg spacetime.py:434-481): each slab
+    is assembled on the device with the previous slab's solution as the
+    time-jump data; returns (per-slab coefficient vectors, [(slab, specs)])."""
+    from .assembly import DofMap
+
+    solver = solver or _default_solver
+    solutions, slabs = [], []
+    prev = problem.initial
+    for n in range(time_partition.n_steps):
+        slab, specs = build_slab(spatial_mesh, time_partition.interval(n), degrees, family)
+        matrix, rhs, _ = assemble_slab(slab, problem.coeffs, specs, prev, config, approach, dirichlet_predicate)
+        counts = np.diff(np.concatenate([[0], np.cumsum([s.n_funcs for s in specs])]))
+        dof_map = DofMap(np.concatenate([[0], np.cumsum(counts)]).astype(np.int64))
+        try:
+            vec = np.asarray(solver(matrix, rhs, dof_map))
+        except Exception as exc:
+            raise RuntimeError(f"slab {n}: {exc}") from exc
+        solutions.append(vec)
+        slabs.append((slab, specs))
+        prev = (specs, vec)
+        if dump_path is not None:
+            save_solution_vector(f"{dump_path}.slab{n:04d}.bin", vec)
+    return solutions, slabs

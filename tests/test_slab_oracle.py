@@ -107,3 +107,84 @@ def test_bottom_facet_block_is_scaled_spatial_mass():
     vol = blocks[0] - Kb
     # the volume term sum_q w (d_t phi_j) phi_i is strictly "upper" in time
     assert np.allclose(vol[:3, :3], 0.0, atol=1e-12)
+
+
+# ---------------------------------------------------------------- device engine
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", GOLDEN, ids=lambda p: os.path.basename(p)[:-4])
+def test_slab_engine_reproduces_reference_golden(path):
+    from paper_2007_04881_b200.spacetime import assemble_slab
+
+    slab, coeffs, specs, prev, pred, ref = load_slab_case(path)
+    m, rhs, stats = assemble_slab(slab, coeffs, specs, prev, dirichlet_predicate=pred)
+    assert_parity(m, rhs, ref, _offsets(specs))
+    assert stats.nnz == m.nnz
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,fam", [(0, "PQ"), (1, "PQ"), (2, "PQ"), (3, "PQ"), (4, "PQ"),
+                                   (1, "P"), (3, "P"), (4, "P")])
+def test_slab_engine_degrees_against_oracle(p, fam):
+    from paper_2007_04881_b200.meshgen import voronoi_mesh
+    from paper_2007_04881_b200.spacetime import assemble_slab
+
+    pm = voronoi_mesh(40, seed=3)
+    coeffs, initial = F.slab_heat()
+    slab, specs = build_slab(pm, (0.2, 0.45), p, Family(fam))
+    m, rhs, _ = assemble_slab(slab, coeffs, specs, initial)
+    ref = OS.assemble_slab(pm, 0.2, 0.45, coeffs, specs, initial)
+    assert_parity(m, rhs, ref, _offsets(specs))
+
+
+@pytest.mark.gpu
+def test_slab_engine_rows_partition_and_determinism():
+    """Row-partitioned slab assembly reproduces the monolithic rows bit for bit
+    (distribute.py:200-232 semantics) and repeated runs are bitwise equal."""
+    from paper_2007_04881_b200.meshgen import voronoi_mesh
+    from paper_2007_04881_b200.spacetime import SlabPlan
+
+    pm = voronoi_mesh(60, seed=4)
+    coeffs, initial = F.slab_adv_heat()
+    slab, specs = build_slab(pm, (0.0, 0.1), 2, Family.PQ)
+    full = SlabPlan(slab, coeffs, specs, initial, dirichlet_predicate=F.slab_predicate("slab_adv_heat"))
+    full.run()
+    full.check_flags()
+    v0 = full.values.clone()
+    full.run()
+    full.check_flags()
+    assert bool((full.values == v0).all())
+    rows = np.arange(13, 41)
+    part = SlabPlan(slab, coeffs, specs, initial, row_elements=rows,
+                    dirichlet_predicate=F.slab_predicate("slab_adv_heat"))
+    part.run()
+    part.check_flags()
+    off = full.t["val_off"].cpu().numpy()
+    a, b = int(off[13]), int(off[41])
+    assert np.array_equal(part.values.cpu().numpy(), v0.cpu().numpy()[a:b])
+    ro = full.t["row_off"].cpu().numpy()
+    rp = full.row_ptr.cpu().numpy()
+    ci = full.col_idx.cpu().numpy()
+    assert np.array_equal(part.col_idx.cpu().numpy(), ci[a:b])
+    d0, d1 = int(full.dof.offsets[13]), int(full.dof.offsets[41])
+    assert np.array_equal(part.rhs.cpu().numpy()[d0:d1], full.rhs.cpu().numpy()[d0:d1])
+    assert int(ro[41] - ro[13]) == part.n_local_rows and rp[-1] == full.nnz
+
+
+@pytest.mark.gpu
+def test_march_two_slabs_against_oracle():
+    """march (spacetime.py:434-481): the second slab's time jump uses the
+    first slab's solution; both systems match the oracle."""
+    from paper_2007_04881_b200.spacetime import ParabolicProblem, TimePartition, assemble_slab, march
+
+    pm = agglomerate(F.square_grid(6), F.grown_clusters(F.square_grid(6), 9, seed=3))
+    coeffs, initial = F.slab_heat()
+    prob = ParabolicProblem(2, coeffs, initial, 0.5)
+    sols, slabs = march(pm, TimePartition.uniform(0.5, 2), prob, 1, Family.PQ)
+    assert len(sols) == 2
+    slab2, specs2 = slabs[1]
+    m, rhs, _ = assemble_slab(slab2, coeffs, specs2, (slabs[0][1], sols[0]))
+    ref = OS.assemble_slab(pm, slab2.t0, slab2.t1, coeffs, specs2, (slabs[0][1], sols[0]))
+    assert_parity(m, rhs, ref, _offsets(specs2))
+    # the discrete solution approximates u = sin sin (1 - t) at the slab end
+    assert np.all(np.isfinite(sols[1]))
