@@ -483,8 +483,16 @@ _CFN = {OP_SIN: "sin", OP_COS: "cos", OP_EXP: "exp", OP_LOG: "log", OP_SQRT: "sq
 _COP = {OP_ADD: "+", OP_SUB: "-", OP_MUL: "*", OP_DIV: "/"}
 
 
-def cuda_expr(e: Expr) -> str:
-    """C expression with the same operation order as the numpy evaluation."""
+def cuda_expr(e: Expr, sinpi: bool = True) -> str:
+    """C expression with the same operation order as the numpy evaluation.
+
+    ``sinpi``: sin/cos of (k*pi)*u are emitted as sinpi/cospi(k*u) -- the
+    same value up to the rounding of k*pi*u (<= 1 ulp of the argument),
+    without the pi/2 argument reduction of sin/cos.  Off = the reference's
+    own sin(fl(k*pi*u)), bit-for-bit in the argument: needed where data is
+    evaluated on a boundary that is a zero of the field (sin(fl(pi)) =
+    1.2e-16, not 0) and a large penalty amplifies it (slab Dirichlet data)."""
+    rec = lambda x: cuda_expr(x, sinpi)
     if e.op == OP_CONST:
         v = float(e.value)
         if not np.isfinite(v):
@@ -492,17 +500,26 @@ def cuda_expr(e: Expr) -> str:
         return f"({v!r})"
     if e.op == OP_COORD:
         return f"x[{int(e.value)}]"
+    if sinpi and e.op in (OP_SIN, OP_COS) and e.args[0].op == OP_MUL:
+        a, b = e.args[0].args
+        for c, u in ((a, b), (b, a)):
+            if c.op == OP_CONST:
+                k = _pi_multiple(float(c.value))
+                if k is not None:
+                    fn = "sinpi" if e.op == OP_SIN else "cospi"
+                    arg = rec(u) if k == 1 else f"({float(k)!r} * {rec(u)})"
+                    return f"{fn}({arg})"
     if e.op in _COP:
-        return f"({cuda_expr(e.args[0])} {_COP[e.op]} {cuda_expr(e.args[1])})"
+        return f"({rec(e.args[0])} {_COP[e.op]} {rec(e.args[1])})"
     if e.op == OP_POW:
         base, ex = e.args
         if ex.op == OP_CONST and float(ex.value) == 2.0:  # numpy squares exactly
-            b = cuda_expr(base)
+            b = rec(base)
             return f"({b} * {b})"
-        return f"pow({cuda_expr(base)}, {cuda_expr(ex)})"
+        return f"pow({rec(base)}, {rec(ex)})"
     if e.op == OP_NEG:
-        return f"(-{cuda_expr(e.args[0])})"
-    return f"{_CFN[e.op]}({cuda_expr(e.args[0])})"
+        return f"(-{rec(e.args[0])})"
+    return f"{_CFN[e.op]}({rec(e.args[0])})"
 
 
 def policy_source(coeffs, dim: int, initial=None) -> str:
@@ -517,7 +534,7 @@ def policy_source(coeffs, dim: int, initial=None) -> str:
 def slab_policy(coeffs, initial=None):
     """(policy source, shared-memory table rows) of a space-time slab
     (coordinates (x, y, t)); the rows follow ``slab_rows`` in slab_body.cuh."""
-    src, info = _policy(coeffs, 3, initial)
+    src, info = _policy(coeffs, 3, initial, sinpi=False)
     kind, diag, n_act = info["kind"], info["diag"], info["n_active"]
     vol = 0 if kind == 0 else (n_act if diag else 6)
     has_vr = info["adv"] or info["reac"]
@@ -529,7 +546,8 @@ def _is_zero(e) -> bool:
     return e is not None and e.is_constant and float(e.value) == 0.0
 
 
-def _policy(coeffs, dim: int, initial=None):
+def _policy(coeffs, dim: int, initial=None, sinpi: bool = True):
+    cuda_expr_ = lambda e: cuda_expr(e, sinpi)
     ten = as_tensor(coeffs.diffusion, dim, "diffusion")
     kind, ent = 0, None
     if ten is not None:
@@ -571,25 +589,25 @@ def _policy(coeffs, dim: int, initial=None):
     bzc = " ".join(f"case {i}: return true;" for i in range(dim) if bnz[i])
     out.append(f"  __device__ static constexpr bool b_nz(int i) "
                f"{{ switch (i) {{ {bzc} default: break; }} return false; }}")
-    iso = cuda_expr(ent) if kind == 1 else "1.0"
+    iso = cuda_expr_(ent) if kind == 1 else "1.0"
     out.append(f"  __device__ double a_iso(const double* x) const {{ return {iso}; }}")
     cases = ""
     if kind == 2:
-        cases = " ".join(f"case {k}: return {cuda_expr(e)};" for k, e in enumerate(ent))
+        cases = " ".join(f"case {k}: return {cuda_expr_(e)};" for k, e in enumerate(ent))
     elif kind == 1:  # the slab kernel reads A entrywise
         cases = " ".join(f"case {i * dim + i}: return {iso};" for i in range(dim))
     out.append(f"  __device__ double a_ij(int i, int j, const double* x) const "
                f"{{ switch (i * {dim} + j) {{ {cases} default: break; }} return 0.0; }}")
     cases = ""
     if adv is not None:
-        cases = " ".join(f"case {k}: return {cuda_expr(e)};" for k, e in enumerate(adv))
+        cases = " ".join(f"case {k}: return {cuda_expr_(e)};" for k, e in enumerate(adv))
     out.append(f"  __device__ double b_i(int i, const double* x) const "
                f"{{ switch (i) {{ {cases} default: break; }} return 0.0; }}")
     for n in ("c", "f", "gD", "gN"):
-        body = cuda_expr(sc[n]) if sc[n] is not None else "0.0"
+        body = cuda_expr_(sc[n]) if sc[n] is not None else "0.0"
         out.append(f"  __device__ double {n}(const double* x) const {{ return {body}; }}")
     out.append(f"  __device__ double u0(const double* x) const "
-               f"{{ return {cuda_expr(u0) if u0 is not None else '0.0'}; }}")
+               f"{{ return {cuda_expr_(u0) if u0 is not None else '0.0'}; }}")
     out.append("};")
     info = dict(kind=kind, diag=diag, n_active=sum(nz[i][i] for i in range(dim)),
                 adv=adv is not None, reac=sc["c"] is not None, src=sc["f"] is not None)
@@ -604,32 +622,3 @@ def _pi_multiple(v: float):
     return None
 
 
-_cuda_expr_plain = cuda_expr
-
-
-def cuda_expr(e: Expr) -> str:  # noqa: F811  (extends the plain lowering)
-    """As the plain lowering, with sin/cos of (k*pi)*u emitted as sinpi/cospi(k*u):
-    the same value up to the rounding of k*pi*u (<= 1 ulp of the argument),
-    without the pi/2 argument reduction of sin/cos."""
-    if e.op in (OP_SIN, OP_COS) and e.args[0].op == OP_MUL:
-        a, b = e.args[0].args
-        for c, u in ((a, b), (b, a)):
-            if c.op == OP_CONST:
-                k = _pi_multiple(float(c.value))
-                if k is not None:
-                    fn = "sinpi" if e.op == OP_SIN else "cospi"
-                    arg = cuda_expr(u) if k == 1 else f"({float(k)!r} * {cuda_expr(u)})"
-                    return f"{fn}({arg})"
-    if e.op in _COP:
-        return f"({cuda_expr(e.args[0])} {_COP[e.op]} {cuda_expr(e.args[1])})"
-    if e.op == OP_POW:
-        base, ex = e.args
-        if ex.op == OP_CONST and float(ex.value) == 2.0:
-            b = cuda_expr(base)
-            return f"({b} * {b})"
-        return f"pow({cuda_expr(base)}, {cuda_expr(ex)})"
-    if e.op == OP_NEG:
-        return f"(-{cuda_expr(e.args[0])})"
-    if e.op in _CFN:
-        return f"{_CFN[e.op]}({cuda_expr(e.args[0])})"
-    return _cuda_expr_plain(e)
