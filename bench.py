@@ -33,6 +33,14 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fp64 SIPG assembly elements/s"
 UNIT = "elements/s"
+SLAB_INTERVAL = (0.0, 0.1)
+# the paper's Approach-2 fp64 single-GPU space-time numbers, s per 10^6 DoFs,
+# p = 1..5 (1x Tesla P100): total kernels / total assembly
+PAPER_P100_S_PER_MDOF = {"kernels": [0.03, 0.17, 0.57, 1.9, 5.5], "total": [1.02, 1.9, 3.7, 7.2, 14.7]}
+
+
+def is_slab(w) -> bool:
+    return w.coeffs.startswith("slab")
 
 
 def _env_int(k, d):
@@ -182,21 +190,40 @@ class CpuReference:
             sw = replace(w, n=max(256, min(w.n, per_core * self.cores)))
         else:
             sw = replace(w, n=12, k=max(300, min(w.k, per_core * self.cores // 2)))
+        self.slab = is_slab(w)
+        if self.slab:
+            per_core = max(8, per_core // (4 * w.degree))
+            sw = replace(w, n=max(128, min(w.n, per_core * self.cores)))
         self.pm = build_mesh(sw)
+        self.w = w
+        if self.slab:
+            from oracle import spacetime as ost
+            from paper_2007_04881_b200 import Family
+            from paper_2007_04881_b200.problems import slab_coefficients
+            from paper_2007_04881_b200.spacetime import build_slab
+
+            self.ost = ost
+            self.coeffs, self.initial = slab_coefficients("heat")
+            _, self.specs = build_slab(self.pm, SLAB_INTERVAL, w.degree, Family.P)
+            return
         self.coeffs = coefficients(w.coeffs, w.dim)
         classify_boundary_faces(self.pm, self.coeffs)
         self.specs = build_basis(self.pm, w.degree)
-        self.w = w
 
     def step(self) -> float:
         t0 = time.perf_counter()
-        self.oracle.assemble(self.pm, self.coeffs, self.specs, workers=self.cores)
+        if self.slab:
+            self.ost.assemble_slab(self.pm, SLAB_INTERVAL[0], SLAB_INTERVAL[1], self.coeffs, self.specs,
+                                   self.initial, workers=self.cores)
+        else:
+            self.oracle.assemble(self.pm, self.coeffs, self.specs, workers=self.cores)
         return time.perf_counter() - t0
 
     def sample(self, dt) -> str:
         kind = "Voronoi" if self.w.dim == 2 else "agglomerated Kuhn"
+        what = "spacetime.assemble_slab" if self.slab else "assemble_approach2"
         return (f"{self.pm.n_elements} elements of the same {kind} generator (p={self.w.degree}, "
-                f"{self.w.coeffs}); oracle/ numpy port of polydg assemble_approach2 with "
+                f"{self.w.coeffs}); oracle/ numpy port of polydg {what} with "
                 f"{self.cores} fork workers, {dt:.2f} s per assembly; elements/s rate-extrapolated "
                 f"to the {self.w.name} workload")
 
@@ -264,17 +291,31 @@ def run_ours(args, w, rank, world, local_rank):
         t0 = time.perf_counter()
         pm = cached_mesh(w)
         mesh_s = time.perf_counter() - t0
-    coeffs = coefficients(w.coeffs, w.dim)
-    classify_boundary_faces(pm, coeffs)
-    specs = build_basis(pm, w.degree)
+    slab_case = is_slab(w)
     cfg = AssemblyConfig()
+    if slab_case:
+        from paper_2007_04881_b200 import Family
+        from paper_2007_04881_b200.problems import slab_coefficients
+        from paper_2007_04881_b200.roofline import slab_work
+        from paper_2007_04881_b200.spacetime import SlabPlan, build_slab
+
+        coeffs, initial = slab_coefficients("heat")
+        slab, specs = build_slab(pm, SLAB_INTERVAL, w.degree, Family.P)
+    else:
+        coeffs = coefficients(w.coeffs, w.dim)
+        classify_boundary_faces(pm, coeffs)
+        specs = build_basis(pm, w.degree)
     rows = None
     if world > 1:
         part = contiguous_partition(pm, world, quadrature_cost_weights(pm, specs))
         rows = part.owned[rank]
     stream = torch.cuda.Stream(dev)
-    plan = SipgPlan(pm, coeffs, specs, cfg, row_elements=rows, device=dev, stream=stream)
-    work = assembly_work(plan)
+    if slab_case:
+        plan = SlabPlan(slab, coeffs, specs, initial, cfg, row_elements=rows, device=dev, stream=stream)
+        work = slab_work(plan)
+    else:
+        plan = SipgPlan(pm, coeffs, specs, cfg, row_elements=rows, device=dev, stream=stream)
+        work = assembly_work(plan)
     lib = _lib.load()
 
     # warm-up (first run also validates the device error flags)
@@ -354,11 +395,13 @@ def run_ours(args, w, rank, world, local_rank):
     achieved = work["flops"] / (ms_el * 1e-3) / 1e12
     gbs = work["bytes"] / (ms_el * 1e-3) / 1e9
     line = {
-        "metric": METRIC, "value": n_el / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
+        "metric": METRIC if not slab_case else "fp64 space-time slab assembly elements/s",
+        "value": n_el / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated mesh; analytic coefficients)",
         "config": {"workload": w.description, "name": w.name, "elements": n_el, "degree": w.degree,
+                   "family": "P" if slab_case else None,
                    "dofs": int(plan.dof.n_dofs), "nnz": int(plan.nnz) if world == 1 else None,
                    "parallelism": f"row-partitioned x{world}" if world > 1 else "single GPU",
                    "l2": "inputs+outputs >> 126 MB L2 (CSR written fresh each step), no flush needed"
@@ -367,7 +410,8 @@ def run_ours(args, w, rank, world, local_rank):
         "phases_ms": {"index": ms_index, "prepass": ms_pre, "element_kernel": ms_el},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(w.name, n_el),
-                     "kernel": "assemble_elements (fused volume+face+boundary, DMMA f64)",
+                     "kernel": "pdg_slab_kernel (fused prism volume+lateral+bottom, DMMA f64)" if slab_case
+                     else "assemble_elements (fused volume+face+boundary, DMMA f64)",
                      "algorithmic_flops_per_launch": work["flops"],
                      "algorithmic_bytes_per_launch": work["bytes"],
                      "hbm_achieved_gbs": gbs, "hbm_peak_gbs": hbm, "hbm_frac": gbs / hbm,
@@ -376,6 +420,14 @@ def run_ours(args, w, rank, world, local_rank):
         "gpu_launches": int(round(launches_tot * K)),
         "gpu_launches_per_step": launches_tot,
     }
+    if slab_case:
+        mdof = plan.dof.n_dofs / 1e6
+        line["s_per_million_dofs"] = {"total": ms_max * 1e-3 / mdof, "kernels": (ms_pre + ms_el) * 1e-3 / mdof,
+                                      "index": ms_index * 1e-3 / mdof}
+        if 1 <= w.degree <= 5:
+            line["paper_p100_s_per_million_dofs"] = {
+                k: v[w.degree - 1] for k, v in PAPER_P100_S_PER_MDOF.items()}
+            line["paper_p100_source"] = "PAPER.md:671-677 (Approach 2, fp64, 1x Tesla P100, not this metric's hardware)"
     if e2e_max is not None:
         line["e2e"] = {"value": n_el / (e2e_max * 1e-3), "unit": UNIT, "ms_per_step": e2e_max,
                        "h2d_bytes_per_step": int(h2d_tot), "d2h_bytes_per_step": int(d2h_tot)}

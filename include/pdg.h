@@ -312,8 +312,10 @@ int pdg_jit_prepare(const pdg_coeffs* coeffs, const char* policy_source, int32_t
  * pdg_pattern_offsets with the slab basis), as are the spatial affine frames
  * (pdg_frames_build).  policy_source: model.slab_policy (coefficients in
  * (x, y, t) + initial data).  Spatial dimension 2 (prisms in 3D), degree
- * <= PDG_SLAB_MAX_DEGREE, uniform degree for family PQ. */
-#define PDG_SLAB_MAX_DEGREE 4
+ * <= PDG_SLAB_MAX_DEGREE (family P) / PDG_SLAB_MAX_DEGREE_PQ, uniform degree
+ * for family PQ. */
+#define PDG_SLAB_MAX_DEGREE 5
+#define PDG_SLAB_MAX_DEGREE_PQ 4
 
 /* Compile (or fetch) the slab kernels of one coefficient set / degree / family. */
 int pdg_slab_prepare(const char* policy_source, int32_t max_degree, int32_t family);

@@ -95,7 +95,7 @@ class Slab(C.Structure):
                 ("prev_dof_offset", _p), ("prev_box", _p), ("family", _i32), ("table_rows", _i32)]
 
 
-SLAB_MAX_DEGREE = 4  # include/pdg.h PDG_SLAB_MAX_DEGREE
+SLAB_MAX_DEGREE = {"P": 5, "PQ": 4}  # include/pdg.h PDG_SLAB_MAX_DEGREE(_PQ)
 
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
 EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes", "pdg_adjacency",

@@ -378,9 +378,10 @@ static std::string slab_source(const std::string& policy, int P, int fam, int nw
 }
 
 static std::string slab_module(const char* policy, int P, int fam, CUmod& mod) {
-  if (P < 0 || P > PDG_SLAB_MAX_DEGREE)
-    return "slab degree " + std::to_string(P) + " outside the supported range 0.." +
-           std::to_string(PDG_SLAB_MAX_DEGREE);
+  const int pmax = fam ? PDG_SLAB_MAX_DEGREE_PQ : PDG_SLAB_MAX_DEGREE;
+  if (P < 0 || P > pmax)
+    return "slab degree " + std::to_string(P) + " outside the supported range 0.." + std::to_string(pmax) +
+           (fam ? " (family PQ)" : " (family P)");
   return get_module(slab_source(policy, P, fam, slab_warps()), mod);
 }
 

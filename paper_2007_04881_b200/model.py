@@ -531,15 +531,15 @@ def policy_source(coeffs, dim: int, initial=None) -> str:
     return _policy(coeffs, dim, initial)[0]
 
 
-def slab_policy(coeffs, initial=None):
-    """(policy source, shared-memory table rows) of a space-time slab
+def slab_policy(coeffs, initial=None, with_info=False):
+    """(policy source, shared-memory table rows[, info]) of a space-time slab
     (coordinates (x, y, t)); the rows follow ``slab_rows`` in slab_body.cuh."""
     src, info = _policy(coeffs, 3, initial, sinpi=False)
     kind, diag, n_act = info["kind"], info["diag"], info["n_active"]
     vol = 0 if kind == 0 else (n_act if diag else 6)
     has_vr = info["adv"] or info["reac"]
     vol += 2 if has_vr else (1 if info["src"] else 0)
-    return src, max(vol, 4)
+    return (src, max(vol, 4), info) if with_info else (src, max(vol, 4))
 
 
 def _is_zero(e) -> bool:
@@ -610,7 +610,8 @@ def _policy(coeffs, dim: int, initial=None, sinpi: bool = True):
                f"{{ return {cuda_expr_(u0) if u0 is not None else '0.0'}; }}")
     out.append("};")
     info = dict(kind=kind, diag=diag, n_active=sum(nz[i][i] for i in range(dim)),
-                adv=adv is not None, reac=sc["c"] is not None, src=sc["f"] is not None)
+                adv=adv is not None, reac=sc["c"] is not None, src=sc["f"] is not None,
+                adv_spatial=any(bnz[: dim - 1]))
     return "\n".join(out), info
 
 

@@ -36,6 +36,24 @@ def coefficients(kind: str, dim: int) -> M.PdeCoefficients:
     raise KeyError(kind)
 
 
+def slab_coefficients(kind: str = "heat"):
+    """Space-time fields in (x, y, t) + initial data of the slab workloads:
+    polydg's parabolic_sine_problem (model.py:277-303), block form
+    diffusion diag(1, 1, 0), advection (0, 0, 1), reaction 1."""
+    X, Y, T = M.X, M.Y, M.Z
+    pi = np.pi
+    if kind != "heat":
+        raise KeyError(kind)
+    s = M.sin(pi * X) * M.sin(pi * Y)
+    coeffs = M.PdeCoefficients(
+        diffusion=M.constant_tensor(np.diag([1.0, 1.0, 0.0])),
+        advection=M.constant_vector([0.0, 0.0, 1.0]),
+        reaction=M.constant_scalar(1.0),
+        source=M.ScalarField(s * ((2.0 * pi ** 2 + 1.0) * (1.0 - T) - 1.0)),
+        dirichlet_data=M.ScalarField(s * (1.0 - T)))
+    return coeffs, M.ScalarField(s)
+
+
 @dataclass(frozen=True)
 class Workload:
     name: str
@@ -63,6 +81,15 @@ WORKLOADS = {
     "cfg5": Workload("cfg5", "2D diffusion (Poisson), p=4, 4M-element Voronoi mesh", 2, 4_000_000, 0, 4,
                      "poisson_sine", 3),
 }
+
+# Space-time slab workloads (the paper's single-GPU tables,
+# one slab of a linear parabolic problem, family P =
+# space-time total degree p, polytopic spatial mesh): prisms over a 2D
+# Voronoi mesh, slab (0, 0.1), sized so the CSR stays well inside HBM.
+for _p, _n in ((1, 1_000_000), (2, 1_000_000), (3, 500_000), (4, 250_000), (5, 125_000)):
+    WORKLOADS[f"st{_p}"] = Workload(
+        f"st{_p}", f"space-time slab, 2D heat (parabolic_sine), family P p={_p}, "
+        f"{_n // 1000}k-prism Voronoi slab", 2, _n, 0, _p, "slab_heat", 5)
 
 
 def build_mesh(w: Workload) -> PolytopicMesh:

@@ -72,3 +72,43 @@ def assembly_work(plan) -> dict:
     bytes_ = 16.0 * nnz + 8.0 * nrows * 2 + geo
     return {"flops": flops, "bytes": bytes_, "flops_volume": vol, "flops_faces": face_int + face_d + face_i,
             "nnz": nnz, "elements": float(owned.sum())}
+
+
+def slab_work(plan) -> dict:
+    """Canonical work of one slab assembly (SpacetimePlan), the counts above
+    with the prism rules: volume sub-prism (p+2)^3 points, lateral sub-facet
+    (p+2)^2, bottom facet (p+2)^2 per sub-triangle (2 n^2 nq, the inflow
+    term); terms: the non-zero diagonal entries of A + [b] + [c]."""
+    from .basis import family_name
+
+    f = plan.flat
+    deg = plan.degrees
+    inc = plan.config.quad_increment
+    n = np.diff(plan.dof.offsets).astype(np.float64)
+    owned = np.zeros(f.n_elements, bool)
+    owned[plan.row_elements] = True
+    info = plan.policy_info
+    items = (info["n_active"] if info["diag"] else 3) * (info["kind"] != 0) + int(info["adv"]) + int(info["reac"])
+    nsim = np.diff(f.elem_ptr).astype(np.float64)
+    m = ((2 * deg + inc + 2) // 2).astype(np.float64)
+    vol = float(np.sum((nsim * 2.0 * n * n * m ** 3 * items)[owned]))
+    bottom = float(np.sum((nsim * 2.0 * n * n * m ** 2)[owned])) if info["adv"] else 0.0
+    nfac = np.diff(f.face_ptr).astype(np.float64)
+    o, nbh = f.face_owner, f.face_neighbor
+    inter = nbh != BOUNDARY
+    nbs = np.where(inter, nbh, 0)
+    pm = np.where(inter, np.maximum(deg[o], deg[nbs]), deg[o])
+    mf = ((2 * pm + inc + 2) // 2).astype(np.float64)
+    nmax = np.where(inter, np.maximum(n[o], n[nbs]), n[o])
+    sides = owned[o].astype(np.float64) + np.where(inter, owned[nbs], False).astype(np.float64)
+    up = 4.0 * float(info["adv_spatial"])
+    face_int = float(np.sum(((16.0 + up) * nmax ** 2 * mf ** 2 * nfac * sides / 2.0)[inter]))
+    tag = plan.lateral_tags
+    dirich = (~inter) & (tag == TAG_CODE["dirichlet"]) & owned[o]
+    face_d = float(np.sum((4.0 * n[o] ** 2 * mf ** 2 * nfac)[dirich]))
+    flops = vol + bottom + face_int + face_d
+    nnz = float(plan.nnz)
+    geo = float(np.sum(nsim[owned])) * 8.0 * 6 + float(np.sum(nfac[inter | owned[o]])) * 40.0
+    bytes_ = 16.0 * nnz + 16.0 * float(plan.n_local_rows) + geo
+    return {"flops": flops, "bytes": bytes_, "flops_volume": vol, "flops_faces": face_int + face_d + bottom,
+            "nnz": nnz, "elements": float(owned.sum()), "family": family_name(plan.family)}

@@ -212,8 +212,9 @@ class SlabPlan:
         if boxes.shape[1:] != (2, 3):
             raise ValueError("slab spec boxes must be (2, 3): spatial box x interval")
         pmax = int(deg.max()) if deg.size else 0
-        if pmax > _lib.SLAB_MAX_DEGREE:
-            raise NotImplementedError(f"slab degree {pmax} exceeds the device range (p <= {_lib.SLAB_MAX_DEGREE})")
+        if pmax > _lib.SLAB_MAX_DEGREE[fname]:
+            raise NotImplementedError(f"slab degree {pmax} exceeds the device range "
+                                      f"(p <= {_lib.SLAB_MAX_DEGREE[fname]} for family {fname})")
         if fname == "PQ" and np.any(deg != pmax):
             raise NotImplementedError("family PQ slabs need a uniform degree on the device")
         counts = np.array([num_basis(int(p), 3, fam) for p in deg], np.int64)
@@ -260,7 +261,8 @@ class SlabPlan:
             self.t["prev"] = T(pvec)
             self.t["prev_dof"] = T(np.concatenate([[0], np.cumsum(pcounts)]).astype(np.int64))
             self.t["prev_box"] = T(pbox)
-        self.policy, rows = slab_policy(coeffs, initial)
+        self.policy, rows, self.policy_info = slab_policy(coeffs, initial, with_info=True)
+        self.family = fam
         self.policy = self.policy.encode()
         _lib.check(self.lib.pdg_slab_prepare(self.policy, pmax, 1 if fname == "PQ" else 0))
 
