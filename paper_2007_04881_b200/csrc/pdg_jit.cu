@@ -354,14 +354,20 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
 // ---------------------------------------------------------------------------
 namespace pdg {
 
-// PDG_SLAB_WARPS: warps per CTA of the slab kernel (1, 2 or 4; default 4)
-static int slab_warps() {
-  const char* v = getenv("PDG_SLAB_WARPS");
-  const int w = v ? atoi(v) : 4;
-  return (w == 1 || w == 2 || w == 4) ? w : 4;
-}
-
 static int slab_nb(int P, int fam) { return fam ? (P + 1) * binom(P + 2, 2) : binom(P + 3, 3); }
+
+// PDG_SLAB_WARPS: warps per CTA of the slab kernel (1, 2 or 4); default by the
+// row block's tile count (measured, 200k-prism slabs, family P, r01:
+// p=1 1/2/4 warps 4.47/5.74/10.5 ms, p=2 11.3/15.7/25.5, p=3 36.7/39.9/55.2,
+// p=4 -/148.7/170.7): one warp up to 3x3 tiles, two up to 6x6, else four
+static int slab_warps(int P, int fam) {
+  if (const char* v = getenv("PDG_SLAB_WARPS")) {
+    const int w = atoi(v);
+    if (w == 1 || w == 2 || w == 4) return w;
+  }
+  const int nt = (slab_nb(P, fam) + 7) / 8;
+  return nt <= 3 ? 1 : (nt <= 6 ? 2 : 4);
+}
 
 static std::string slab_source(const std::string& policy, int P, int fam, int nw) {
   std::ostringstream os;
@@ -382,7 +388,7 @@ static std::string slab_module(const char* policy, int P, int fam, CUmod& mod) {
   if (P < 0 || P > pmax)
     return "slab degree " + std::to_string(P) + " outside the supported range 0.." + std::to_string(pmax) +
            (fam ? " (family PQ)" : " (family P)");
-  return get_module(slab_source(policy, P, fam, slab_warps()), mod);
+  return get_module(slab_source(policy, P, fam, slab_warps(P, fam)), mod);
 }
 
 static int slab_check(const pdg_mesh* mesh, const pdg_basis* basis, const char* policy, const pdg_rules* rules,
@@ -409,6 +415,7 @@ static SlabArgs slab_args(const pdg_mesh* mesh, const pdg_basis* basis, const pd
   a.sl = *slab;
   a.sframe = frames->simplex;
   a.fframe = frames->facet;
+  a.erec = frames->element;
   a.sigma = sigma;
   a.flow = flow;
   a.flags = flags;
@@ -462,13 +469,14 @@ extern "C" int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, c
   PDG_TRY {
     int rc = slab_check(mesh, basis, policy_source, rules, params, slab);
     if (rc) return rc;
-    if (!pattern || !frames || !frames->simplex || !frames->facet || !sigma || !face_flow || !values || !rhs)
+    if (!pattern || !frames || !frames->simplex || !frames->facet || !frames->element || !sigma || !face_flow ||
+        !values || !rhs)
       return fail(PDG_ERR_INVALID, "null argument");
     if (!pattern->nbr_ptr || !pattern->nbr_elem || !pattern->nbr_iface || !pattern->row_len ||
         !pattern->elem_val_offset)
       return fail(PDG_ERR_INVALID, "pattern not built (pdg_adjacency / pdg_pattern_offsets)");
     if (pattern->n_row_elements <= 0) return PDG_OK;
-    const int P = basis->max_degree, fam = slab->family, nw = slab_warps();
+    const int P = basis->max_degree, fam = slab->family, nw = slab_warps(P, fam);
     CUmod mod = nullptr;
     std::string err = slab_module(policy_source, P, fam, mod);
     CUfunc fn = nullptr;

@@ -112,6 +112,7 @@ struct SlabArgs {
   pdg_slab sl;
   const double* sframe;  // spatial simplex frames [n_simplices][8], element order
   const double* fframe;  // spatial facet frames [n_facets][8]
+  const double* erec;    // spatial basis constants [n_elements][8] (centre, 1/half, 1/sqrt(width))
   const double* sigma;   // lateral penalty per spatial face
   const int8_t* flow;    // lateral flow side per spatial face
   double* values;
@@ -170,6 +171,24 @@ __device__ __forceinline__ double slab_flux(const CF& cf, const SlabTab<P, PQ>& 
     fl += n[i] * ag;
   }
   return fl;
+}
+
+// prism basis constants: the spatial part from the frame pre-pass records
+// (box_const of the spatial box, pdg_prepass.cu frames_kernel), the time part
+// shared by every prism of the slab
+__device__ __forceinline__ BoxConst<3> slab_box(const double* erec, int64_t e, const BoxConst<1>& tb) {
+  const double* r = erec + e * 8;
+  BoxConst<3> b;
+  b.c[0] = r[0];
+  b.c[1] = r[1];
+  b.ih[0] = r[2];
+  b.ih[1] = r[3];
+  b.rs[0] = r[4];
+  b.rs[1] = r[5];
+  b.c[2] = tb.c[0];
+  b.ih[2] = tb.ih[0];
+  b.rs[2] = tb.rs[0];
+  return b;
 }
 
 template <int TR, int TC>
@@ -267,13 +286,18 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
   double* const r2_ = sc + 160;       // RHS weight of the F row
   const double t0 = a.sl.t0, tau = a.sl.t1 - a.sl.t0;
   const bool grad_terms = CF::diff_kind() != PDG_DIFF_NONE && a.prm.include_gradient_terms;
+  BoxConst<1> tbox;  // time axis of every prism box: (t0, t1)
+  {
+    const double tt[2] = {a.sl.t0, a.sl.t1};
+    tbox = box_const<1>(tt);
+  }
 
   for (int64_t k = blockIdx.x; k < pat.n_row_elements; k += gridDim.x) {
     const int32_t e = pat.row_elements ? pat.row_elements[k] : (int32_t)k;
     const int pe = B.degree[e];
     const int64_t dof_e = B.dof_offset[e];
     const int ne = (int)(B.dof_offset[e + 1] - dof_e);
-    const BoxConst<3> bx = box_const<3>(B.box + (int64_t)e * 6);
+    const BoxConst<3> bx = slab_box(a.erec, e, tbox);
     const int64_t voff = pat.elem_val_offset[k];
     const int64_t Lrow = pat.row_len[k];
     const int64_t q0 = pat.nbr_ptr[e];
@@ -520,7 +544,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
       if (j == e) continue;
       const int ifc = nb_if[qn];
       const int pj = B.degree[j];
-      const BoxConst<3> bo = box_const<3>(B.box + (int64_t)j * 6);
+      const BoxConst<3> bo = slab_box(a.erec, j, tbox);
       const int order = 2 * max(pe, pj) + a.prm.quad_increment;
       const int r0e = R.face_offset[order], nqe = R.face_count[order];
       const int nqf = nqe * nqe;  // edge rule x time rule of the same order

@@ -211,6 +211,9 @@ class SlabPlan:
             raise AssemblyError("one BasisSpec per element required")
         if boxes.shape[1:] != (2, 3):
             raise ValueError("slab spec boxes must be (2, 3): spatial box x interval")
+        if not (np.all(boxes[:, 0, 2] == slab.t0) and np.all(boxes[:, 1, 2] == slab.t1)):
+            raise NotImplementedError("the device slab engine needs prism boxes with the slab's time "
+                                      "interval (build_slab)")
         pmax = int(deg.max()) if deg.size else 0
         if pmax > _lib.SLAB_MAX_DEGREE[fname]:
             raise NotImplementedError(f"slab degree {pmax} exceeds the device range "
