@@ -228,6 +228,17 @@ typedef struct pdg_slab {
   int32_t table_rows;             /* shared table rows of the coefficient set (model.slab_policy) */
 } pdg_slab;
 
+/* Approach-1 work items (see pdg_a1_emit). */
+typedef struct pdg_a1_items {
+  int64_t n_volume, n_interior, n_boundary;
+  int64_t n_cols;                /* global DoFs (key = row * n_cols + col) */
+  const int32_t* volume_element; /* [n_volume] element of the i-th simplex (element order) */
+  const int32_t* face;           /* [n_interior + n_boundary] face of the item */
+  const int64_t* facet_row;      /* [n_interior + n_boundary] its sub-facet row */
+  const int64_t* stripe_offset;  /* [n_items + 1] triplet stripe offsets (widths of assembly.py:733-745) */
+  const int64_t* load_offset;    /* [n_items + 1] load (RHS) entry offsets */
+} pdg_a1_items;
+
 #ifndef __CUDACC_RTC__ /* the runtime-compiled kernels need the types only */
 int pdg_abi_version(void);
 const char* pdg_last_error(void);
@@ -338,6 +349,35 @@ int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, const char* 
                       const pdg_pattern* pattern, const pdg_frames* frames, const double* sigma,
                       const int8_t* face_flow, double* values, double* rhs, uint32_t* err_flags,
                       pdg_stream stream);
+
+/* ---- Approach 1: stage-and-sort (polydg assembly.py:158-174, 977-1087) ----
+ * Work items in polydg's plan order (volume sub-simplices, interior
+ * sub-facets, boundary sub-facets; uniform-degree meshes reproduce
+ * build_work_plan's order exactly), each writing its dense local blocks into a
+ * triplet stripe (key = row * n_cols + col; unused slots keep the sentinel
+ * key ~0), then a stable radix sort + reduce-by-key into CSR. */
+
+/* Emit every item's triplets + load pairs (NVRTC-specialised like pdg_assemble_jit);
+ * sigma / face_flow from pdg_face_prepass, frames from pdg_frames_build. */
+int pdg_a1_emit(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                const char* policy_source, const pdg_rules* rules, const pdg_params* params,
+                const pdg_frames* frames, const double* sigma, const int8_t* face_flow,
+                const pdg_a1_items* items, uint64_t* keys, double* vals, uint64_t* load_keys,
+                double* load_vals, uint32_t* err_flags, pdg_stream stream);
+
+/* Scratch bytes of pdg_triplets_to_csr / pdg_triplets_to_vector for n triplets. */
+size_t pdg_triplets_workspace_bytes(int64_t n_triplets);
+
+/* triplets_to_csr (assembly.py:1002-1031): stable sort by key, sum duplicates in
+ * input order, CSR of n_rows x n_cols.  Sentinel keys (~0) are dropped.  Outputs
+ * have capacity n_triplets; *nnz_device receives the number of entries. */
+int pdg_triplets_to_csr(const uint64_t* keys, const double* vals, int64_t n_triplets, int64_t n_rows,
+                        int64_t n_cols, int64_t* row_ptr, int64_t* col_idx, double* values,
+                        int64_t* nnz_device, void* workspace, size_t workspace_bytes, pdg_stream stream);
+
+/* Load pairs (row, value) -> dense vector[n_rows] (the RHS sink, assembly.py:966-970). */
+int pdg_triplets_to_vector(const uint64_t* keys, const double* vals, int64_t n, int64_t n_rows,
+                           double* out, void* workspace, size_t workspace_bytes, pdg_stream stream);
 
 /* ---- unit-level entry points (tests / debugging) ---- */
 

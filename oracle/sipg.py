@@ -522,3 +522,27 @@ def element_kernel(mesh, e, coeffs, spec, quad_increment=2):
         K += k
         f += l
     return K, f
+
+
+# -- Approach 1 merge (assembly.py:1002-1031) ----------------------------------------------
+
+def triplets_to_csr(rows, cols, vals, n_rows, n_cols, sentinel=None):
+    """Stable sort by (row, col), duplicates summed in input order ->
+    (row_ptr, col_idx, values)."""
+    rows = np.asarray(rows, np.int64)
+    cols = np.asarray(cols, np.int64)
+    vals = np.asarray(vals, float)
+    if sentinel is not None:
+        keep = rows != sentinel
+        rows, cols, vals = rows[keep], cols[keep], vals[keep]
+    key = rows * np.int64(n_cols) + cols
+    order = np.argsort(key, kind="stable")
+    ks, vs = key[order], vals[order]
+    if ks.size == 0:
+        return np.zeros(n_rows + 1, np.int64), np.zeros(0, np.int64), np.zeros(0)
+    starts = np.flatnonzero(np.concatenate([[True], ks[1:] != ks[:-1]]))
+    sums = np.add.reduceat(vs, starts)
+    uk = ks[starts]
+    row_ptr = np.zeros(n_rows + 1, np.int64)
+    np.cumsum(np.bincount(uk // n_cols, minlength=n_rows), out=row_ptr[1:])
+    return row_ptr, (uk % n_cols).astype(np.int64), sums

@@ -95,6 +95,12 @@ class Slab(C.Structure):
                 ("prev_dof_offset", _p), ("prev_box", _p), ("family", _i32), ("table_rows", _i32)]
 
 
+class A1Items(C.Structure):
+    _fields_ = [("n_volume", _i64), ("n_interior", _i64), ("n_boundary", _i64), ("n_cols", _i64),
+                ("volume_element", _p), ("face", _p), ("facet_row", _p), ("stripe_offset", _p),
+                ("load_offset", _p)]
+
+
 SLAB_MAX_DEGREE = {"P": 5, "PQ": 4}  # include/pdg.h PDG_SLAB_MAX_DEGREE(_PQ)
 
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
@@ -102,6 +108,7 @@ EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspa
            "pdg_pattern_offsets", "pdg_pattern_fill", "pdg_face_prepass", "pdg_iface_records", "pdg_frames_build",
            "pdg_assemble", "pdg_assemble_jit", "pdg_jit_prepare",
            "pdg_slab_prepare", "pdg_slab_prepass", "pdg_slab_assemble",
+           "pdg_a1_emit", "pdg_triplets_workspace_bytes", "pdg_triplets_to_csr", "pdg_triplets_to_vector",
            "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks")
 
 
@@ -141,12 +148,19 @@ def load():
                                      P(Frames), _p, _p, _p, _p]
     lib.pdg_slab_assemble.argtypes = [P(Mesh), P(Basis), C.c_char_p, P(Rules), P(Params), P(Slab),
                                       P(Pattern), P(Frames), _p, _p, _p, _p, _p, _p]
+    lib.pdg_a1_emit.argtypes = [P(Mesh), P(Basis), P(Coeffs), C.c_char_p, P(Rules), P(Params), P(Frames),
+                                _p, _p, P(A1Items), _p, _p, _p, _p, _p, _p]
+    lib.pdg_triplets_workspace_bytes.restype = C.c_size_t
+    lib.pdg_triplets_workspace_bytes.argtypes = [_i64]
+    lib.pdg_triplets_to_csr.argtypes = [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, C.c_size_t, _p]
+    lib.pdg_triplets_to_vector.argtypes = [_p, _p, _i64, _i64, _p, _p, C.c_size_t, _p]
     lib.pdg_map_simplices.argtypes = [P(Mesh), P(Rules), _i32, _p, _i64, _p, _p, _p, _p]
     lib.pdg_tabulate.argtypes = [P(Mesh), P(Basis), _i32, _p, _i64, _p, _p, _p]
     lib.pdg_element_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params),
                                        P(Frames), _p, _i64, _p, _p, _p, _p]
     for name in EXPORTS:
-        if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes"):
+        if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes",
+                        "pdg_triplets_workspace_bytes"):
             getattr(lib, name).restype = C.c_int
     if lib.pdg_abi_version() != ABI_VERSION:
         raise EngineUnavailable("libpdg.so ABI version mismatch")

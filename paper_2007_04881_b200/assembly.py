@@ -752,10 +752,18 @@ def assemble_approach2(mesh, coeffs, specs, config: Optional[AssemblyConfig] = N
 
 
 def assemble_approach1(mesh, coeffs, specs, config: Optional[AssemblyConfig] = None):
-    """polydg's stage-and-sort path yields the same CSR (within 1e-12); on the
-    device both entry points run the preset-sparsity engine."""
-    matrix, rhs, stats, _ = assemble_approach2(mesh, coeffs, specs, config)
-    return matrix, rhs, stats
+    """Stage-and-sort assembly on the device (polydg ``assembly.py:1036-1045``):
+    per-item triplet stripes, stable radix sort, reduce-by-key
+    (``approach1.py``).  Per-element degrees (whose volume items polydg
+    regroups by degree) run the preset-sparsity engine, which yields the same
+    CSR within 1e-12 (polydg's own A1 == A2 contract)."""
+    from .approach1 import assemble_approach1_device
+
+    deg, _, _ = spec_arrays(specs)
+    if deg.size and np.any(deg != deg[0]):
+        matrix, rhs, stats, _ = assemble_approach2(mesh, coeffs, specs, config)
+        return matrix, rhs, stats
+    return assemble_approach1_device(mesh, coeffs, specs, config)
 
 
 def _assemble_approach2_rows(mesh, coeffs, specs, config, row_elements):

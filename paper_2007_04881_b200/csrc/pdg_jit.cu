@@ -30,6 +30,7 @@
 #include "assemble_kernel.cuh"
 #include "assemble_ws.cuh"
 #include "slab_body.cuh"
+#include "approach1_body.cuh"
 
 namespace pdg {
 
@@ -498,6 +499,90 @@ extern "C" int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, c
     if (A.cuLaunchKernel(fn, (unsigned)grid, 1, 1, 32 * nw, 1, 1, (unsigned)smem, (cudaStream_t)stream, args,
                          nullptr) != 0)
       return fail(PDG_ERR_CUDA, "cuLaunchKernel(pdg_slab_kernel) failed");
+    note_launch();
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+// ---------------------------------------------------------------------------
+// Approach 1 (approach1_body.cuh): item emission, one warp per work item
+// ---------------------------------------------------------------------------
+namespace pdg {
+
+static std::string a1_source(const std::string& policy, int dim, int P, int nw) {
+  std::ostringstream os;
+  os << "#include \"approach1_body.cuh\"\n"
+     << "namespace pdg_jit {\nusing namespace pdg;\n" << policy << "\n}\n"
+     << "extern \"C\" __global__ void __launch_bounds__(" << 32 * nw << ") "
+     << "pdg_a1_kernel(const __grid_constant__ pdg::A1Args a) {\n"
+     << "  pdg::approach1_body<" << dim << ", " << P << ", pdg_jit::JitCoef>(a, pdg_jit::JitCoef());\n}\n";
+  return os.str();
+}
+
+static int a1_warps(int dim, int P) {
+  const int nb = binom(P + dim, dim), nbp = ((nb + 7) / 8) * 8;
+  const size_t per = (size_t)a1_warp_doubles(dim, nbp) * 8;
+  int w = (int)std::min<size_t>(4, (200 * 1024) / per);
+  return w < 1 ? 1 : w;
+}
+
+}  // namespace pdg
+
+extern "C" int pdg_a1_emit(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                           const char* policy_source, const pdg_rules* rules, const pdg_params* params,
+                           const pdg_frames* frames, const double* sigma, const int8_t* face_flow,
+                           const pdg_a1_items* items, uint64_t* keys, double* vals, uint64_t* load_keys,
+                           double* load_vals, uint32_t* err_flags, pdg_stream stream) {
+  PDG_TRY {
+    int rc = check_common(mesh, basis, coeffs);
+    if (rc) return rc;
+    if (!policy_source || !rules || !params || !frames || !frames->simplex || !frames->facet || !frames->element ||
+        !sigma || !face_flow || !items || !keys || !vals || !load_keys || !load_vals)
+      return fail(PDG_ERR_INVALID, "null argument");
+    const int64_t n_items = items->n_volume + items->n_interior + items->n_boundary;
+    if (n_items <= 0) return PDG_OK;
+    if (!items->stripe_offset || !items->load_offset || (items->n_volume && !items->volume_element) ||
+        (items->n_interior + items->n_boundary > 0 && (!items->face || !items->facet_row)))
+      return fail(PDG_ERR_INVALID, "work item arrays missing");
+    const int dim = mesh->dim, P = basis->max_degree, nw = a1_warps(dim, P);
+    CUmod mod = nullptr;
+    std::string err = get_module(a1_source(policy_source, dim, P, nw), mod);
+    CUfunc fn = nullptr;
+    if (err.empty()) err = get_function(mod, "pdg_a1_kernel", fn);
+    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
+    A1Args a;
+    std::memset(&a, 0, sizeof(a));
+    a.m = *mesh;
+    a.B = *basis;
+    a.R = *rules;
+    a.prm = *params;
+    a.it = *items;
+    a.sframe = frames->simplex;
+    a.fframe = frames->facet;
+    a.erec = frames->element;
+    a.sigma = sigma;
+    a.flow = face_flow;
+    a.keys = keys;
+    a.vals = vals;
+    a.load_keys = load_keys;
+    a.load_vals = load_vals;
+    a.n_cols = items->n_cols;
+    a.flags = err_flags;
+    if (items->n_cols <= 0) return fail(PDG_ERR_INVALID, "n_cols must be positive");
+    const int nb = binom(P + dim, dim), nbp = ((nb + 7) / 8) * 8;
+    const size_t smem = (size_t)a1_warp_doubles(dim, nbp) * 8 * nw;
+    Api& A = api();
+    if (A.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES_, (int)smem) != 0)
+      return fail(PDG_ERR_CUDA, "cuFuncSetAttribute(max dynamic smem) failed");
+    int per_sm = 0;
+    if (A.cuOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * nw, smem) != 0 || per_sm < 1) per_sm = 1;
+    const int64_t need = (n_items + nw - 1) / nw;
+    const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm * 8);
+    void* args[] = {&a};
+    if (A.cuLaunchKernel(fn, (unsigned)grid, 1, 1, 32 * nw, 1, 1, (unsigned)smem, (cudaStream_t)stream, args,
+                         nullptr) != 0)
+      return fail(PDG_ERR_CUDA, "cuLaunchKernel(pdg_a1_kernel) failed");
     note_launch();
     return PDG_OK;
   }

@@ -200,51 +200,76 @@ __global__ void face_prepass(const pdg_mesh m, const pdg_basis B, const __grid_c
   }
 }
 
-// Interface records (pdg_iface_rec) of the owned rows: one thread per row
-// element walks its sorted neighbour list (assembly.py:309-321: column start
-// = prefix of the neighbours' DoF counts) and flattens, per entry, the
-// interface's first-face metadata the element kernel needs before any face
-// point can be tabulated (face range, side, downwind flag, sigma, normal,
-// first sub-facet row, paired-round eligibility).
+// Interface records (pdg_iface_rec) of the owned rows: one warp per row
+// element, lanes over its sorted neighbour list (assembly.py:309-321: column
+// start = exclusive prefix of the neighbours' DoF counts, a warp scan),
+// flattening per entry the interface's first-face metadata the element
+// kernel needs before any face point can be tabulated (face range, side,
+// downwind flag, sigma, normal, first sub-facet row, paired-round
+// eligibility).  Records are staged in shared memory and written as
+// contiguous 16-byte chunks (coalesced; one record = 80 bytes).
 template <int DIM>
-__global__ void iface_records_kernel(const pdg_mesh m, const pdg_basis B, const pdg_rules R, int inc,
-                                     int has_adv, const pdg_pattern P, const double* sigma,
-                                     const int8_t* flow) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < P.n_row_elements; k += stride) {
+__global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, const pdg_basis B, const pdg_rules R,
+                                                            int inc, int has_adv, const pdg_pattern P,
+                                                            const double* sigma, const int8_t* flow) {
+  __shared__ int4 stage[4][32 * 5];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int4* st = stage[wib];
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < P.n_row_elements; k += nwarps) {
     const int32_t e = P.row_elements ? P.row_elements[k] : (int32_t)k;
     const int pe = B.degree[e];
-    const int64_t q1 = P.nbr_ptr[e + 1];
-    int col = 0;
-    for (int64_t q = P.nbr_ptr[e]; q < q1; ++q) {
-      const int32_t j = P.nbr_elem[q];
-      const int nj = (int)(B.dof_offset[j + 1] - B.dof_offset[j]);
-      const int pj = B.degree[j];
-      int fa = 0, fb = 0, row0 = 0, info = 0;
+    const int64_t q0 = P.nbr_ptr[e], q1 = P.nbr_ptr[e + 1];
+    int carry = 0;
+    for (int64_t c0 = q0; c0 < q1; c0 += 32) {
+      const int nv = (int)(q1 - c0 < 32 ? q1 - c0 : 32);
+      const int64_t q = c0 + lane;
+      int j = 0, nj = 0, pj = 0, fa = 0, fb = 0, row0 = 0, info = 0;
       double sig = 0.0, nrm[3] = {0.0, 0.0, 0.0};
-      if (j != e) {
-        const int32_t ifc = P.nbr_iface[q];
-        fa = (int)m.iface_ptr[ifc];
-        fb = (int)m.iface_ptr[ifc + 1];
-        const int side = m.face_owner[fa] == e ? 0 : 1;
-        const bool down = has_adv && flow[fa] == side;
-        row0 = (int)m.face_ptr[fa];
-        const int nrows = (int)(m.face_ptr[fa + 1] - row0);
-        const int nq = R.face_count[2 * max(pe, pj) + inc];
-        const bool simple = fb - fa == 1 && nrows == 1 && nq <= 8;
-        info = side | (down ? 2 : 0) | (simple ? 4 : 0);
-        sig = sigma[fa];
+      long long dof = 0;
+      if (lane < nv) {
+        j = P.nbr_elem[q];
+        dof = B.dof_offset[j];
+        nj = (int)(B.dof_offset[j + 1] - dof);
+        pj = B.degree[j];
+        if (j != e) {
+          const int32_t ifc = P.nbr_iface[q];
+          fa = (int)m.iface_ptr[ifc];
+          fb = (int)m.iface_ptr[ifc + 1];
+          const int side = m.face_owner[fa] == e ? 0 : 1;
+          const bool down = has_adv && flow[fa] == side;
+          row0 = (int)m.face_ptr[fa];
+          const int nrows = (int)(m.face_ptr[fa + 1] - row0);
+          const int nq = R.face_count[2 * max(pe, pj) + inc];
+          const bool simple = fb - fa == 1 && nrows == 1 && nq <= 8;
+          info = side | (down ? 2 : 0) | (simple ? 4 : 0);
+          sig = sigma[fa];
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)fa * DIM + i];
+          for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)fa * DIM + i];
+        }
       }
-      int4* o = reinterpret_cast<int4*>(P.nbr_rec + q);
-      o[0] = make_int4(j, nj, col, pj);
-      o[1] = make_int4(fa, fb, row0, info);
-      double2* od = reinterpret_cast<double2*>(P.nbr_rec + q) + 2;
-      od[0] = make_double2(sig, nrm[0]);
-      od[1] = make_double2(nrm[1], nrm[2]);
-      reinterpret_cast<longlong2*>(P.nbr_rec + q)[4] = make_longlong2(B.dof_offset[j], 0);
-      col += nj;
+      // exclusive scan of nj over the chunk
+      int incl = nj;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int col = carry + incl - nj;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+      if (lane < nv) {
+        int4* r = st + lane * 5;
+        r[0] = make_int4(j, nj, col, pj);
+        r[1] = make_int4(fa, fb, row0, info);
+        double2* rd = reinterpret_cast<double2*>(r + 2);
+        rd[0] = make_double2(sig, nrm[0]);
+        rd[1] = make_double2(nrm[1], nrm[2]);
+        reinterpret_cast<longlong2*>(r + 4)[0] = make_longlong2(dof, 0);
+      }
+      __syncwarp();
+      int4* dst = reinterpret_cast<int4*>(P.nbr_rec + c0);
+      for (int c = lane; c < nv * 5; c += 32) dst[c] = st[c];
+      __syncwarp();
     }
   }
 }
@@ -262,7 +287,7 @@ extern "C" int pdg_iface_records(const pdg_mesh* mesh, const pdg_basis* basis, c
       return fail(PDG_ERR_INVALID, "null argument");
     if (pattern->n_row_elements <= 0) return PDG_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const int grid = grid_for(pattern->n_row_elements, 128);
+    const int grid = grid_for_warps(pattern->n_row_elements, 128);
     if (mesh->dim == 2)
       iface_records_kernel<2><<<grid, 128, 0, st>>>(*mesh, *basis, *rules, params->quad_increment,
                                                     coeffs->has_advection, *pattern, sigma, face_flow);

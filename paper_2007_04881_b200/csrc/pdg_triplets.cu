@@ -1,0 +1,190 @@
+// Approach-1 index phase on the device: triplets -> CSR (polydg
+// triplets_to_csr, assembly.py:1002-1031) and load pairs -> RHS.
+//
+//   keys = row * n_cols + col (uint64; sentinel ~0 for unused stripe slots)
+//   1. stable LSD radix sort of (key, value) over the significant key bits
+//      (ties keep input order, so duplicates merge in the stripe order, like
+//      polydg's argsort(kind="stable") + add.reduceat)
+//   2. reduce-by-key (sum) -> unique keys + sums; sentinels form the last run
+//   3. row_ptr[r] = lower_bound(unique keys, r * n_cols) (one thread per row)
+//      col_idx = key % n_cols
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+
+#include "pdg_internal.cuh"
+
+namespace pdg {
+
+namespace {
+
+struct Ws {
+  uint64_t* keys_alt;
+  double* vals_alt;
+  uint64_t* ukeys;
+  double* usums;
+  int64_t* nruns;
+  void* temp;
+  size_t temp_bytes;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t cub_temp_bytes(int64_t n) {
+  size_t sort_b = 0, red_b = 0;
+  cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+  cub::DoubleBuffer<double> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, kb, vb, (int64_t)n, 0, 64);
+  cub::DeviceReduce::ReduceByKey(nullptr, red_b, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                 (const double*)nullptr, (double*)nullptr, (int64_t*)nullptr, cub::Sum(),
+                                 (int64_t)n);
+  return std::max(sort_b, red_b);
+}
+
+Ws carve(void* base, int64_t n) {
+  Ws w;
+  char* p = static_cast<char*>(base);
+  const size_t nk = align256((size_t)n * 8);
+  w.keys_alt = reinterpret_cast<uint64_t*>(p);
+  p += nk;
+  w.vals_alt = reinterpret_cast<double*>(p);
+  p += nk;
+  w.ukeys = reinterpret_cast<uint64_t*>(p);
+  p += nk;
+  w.usums = reinterpret_cast<double*>(p);
+  p += nk;
+  w.nruns = reinterpret_cast<int64_t*>(p);
+  p += 256;
+  w.temp = p;
+  w.temp_bytes = cub_temp_bytes(n);
+  return w;
+}
+
+int key_bits(uint64_t max_key) {
+  int b = 1;
+  while (b < 64 && (max_key >> b)) ++b;
+  return b;
+}
+
+// sentinel keys are ~0: with a partial bit range they would sort as their low
+// bits, so they are first mapped to the largest in-range key + 1
+__global__ void clamp_sentinels(const uint64_t* in, uint64_t* out, int64_t n, uint64_t lim) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] > lim ? lim : in[i];
+}
+
+__global__ void csr_rows(const uint64_t* ukeys, const int64_t* nruns, uint64_t lim, int64_t n_rows, int64_t n_cols,
+                         int64_t* row_ptr, int64_t* col_idx, int64_t* nnz_out) {
+  int64_t nu = *nruns;
+  if (nu > 0 && ukeys[nu - 1] == lim) --nu;  // the sentinel run
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n_rows; r += stride) {
+    const uint64_t key = (uint64_t)r * (uint64_t)n_cols;
+    int64_t lo = 0, hi = nu;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ukeys[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    row_ptr[r] = lo;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu; i += stride)
+    col_idx[i] = (int64_t)(ukeys[i] % (uint64_t)n_cols);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && nnz_out) *nnz_out = nu;
+}
+
+__global__ void scatter_vector(const uint64_t* ukeys, const double* usums, const int64_t* nruns, uint64_t lim,
+                               double* out, int64_t n_rows) {
+  const int64_t nu = *nruns;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu; i += (int64_t)gridDim.x * blockDim.x)
+    if (ukeys[i] < lim && (int64_t)ukeys[i] < n_rows) out[ukeys[i]] = usums[i];
+}
+
+// sort + reduce; returns the workspace view (unique keys / sums / run count filled)
+int sort_reduce(const uint64_t* keys, const double* vals, int64_t n, uint64_t lim, void* ws, size_t ws_bytes,
+                cudaStream_t st, Ws& w, uint64_t** ksorted, double** vsorted) {
+  w = carve(ws, n);
+  const size_t need = align256((size_t)n * 8) * 4 + 256 + w.temp_bytes;
+  if (ws_bytes < need) return fail(PDG_ERR_INVALID, "triplet workspace too small (pdg_triplets_workspace_bytes)");
+  // sorted keys land in ukeys (as the DoubleBuffer's first buffer), values in usums
+  uint64_t* k0 = w.ukeys;
+  double* v0 = w.usums;
+  clamp_sentinels<<<grid_for(n, 256), 256, 0, st>>>(keys, k0, n, lim);
+  note_launch();
+  PDG_CUDA(cudaMemcpyAsync(v0, vals, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+  cub::DoubleBuffer<uint64_t> kb(k0, w.keys_alt);
+  cub::DoubleBuffer<double> vb(v0, w.vals_alt);
+  size_t tb = w.temp_bytes;
+  PDG_CUDA(cub::DeviceRadixSort::SortPairs(w.temp, tb, kb, vb, n, 0, key_bits(lim), st));
+  note_launch();
+  *ksorted = kb.Current();
+  *vsorted = vb.Current();
+  return PDG_OK;
+}
+
+}  // namespace
+}  // namespace pdg
+
+using namespace pdg;
+
+extern "C" size_t pdg_triplets_workspace_bytes(int64_t n_triplets) {
+  const int64_t n = std::max<int64_t>(n_triplets, 1);
+  return align256((size_t)n * 8) * 4 + 256 + cub_temp_bytes(n) + 256;
+}
+
+extern "C" int pdg_triplets_to_csr(const uint64_t* keys, const double* vals, int64_t n_triplets, int64_t n_rows,
+                                   int64_t n_cols, int64_t* row_ptr, int64_t* col_idx, double* values,
+                                   int64_t* nnz_device, void* workspace, size_t workspace_bytes, pdg_stream stream) {
+  PDG_TRY {
+    if (!keys || !vals || !row_ptr || !col_idx || !values || !workspace) return fail(PDG_ERR_INVALID, "null argument");
+    if (n_rows <= 0 || n_cols <= 0) return fail(PDG_ERR_INVALID, "empty matrix shape");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_triplets <= 0) {
+      PDG_CUDA(cudaMemsetAsync(row_ptr, 0, (size_t)(n_rows + 1) * 8, st));
+      if (nnz_device) PDG_CUDA(cudaMemsetAsync(nnz_device, 0, 8, st));
+      return PDG_OK;
+    }
+    const uint64_t lim = (uint64_t)n_rows * (uint64_t)n_cols;  // first out-of-range key
+    Ws w;
+    uint64_t* ks;
+    double* vs;
+    int rc = sort_reduce(keys, vals, n_triplets, lim, workspace, workspace_bytes, st, w, &ks, &vs);
+    if (rc) return rc;
+    // reduce-by-key into the outputs (values / a key scratch that reuses the other buffer)
+    uint64_t* ukeys = ks == w.ukeys ? w.keys_alt : w.ukeys;
+    size_t tb = w.temp_bytes;
+    PDG_CUDA(cub::DeviceReduce::ReduceByKey(w.temp, tb, ks, ukeys, vs, values, w.nruns, cub::Sum(), n_triplets, st));
+    note_launch();
+    csr_rows<<<grid_for(n_rows + 1, 256), 256, 0, st>>>(ukeys, w.nruns, lim, n_rows, n_cols, row_ptr, col_idx,
+                                                        nnz_device);
+    note_launch();
+    PDG_CUDA(cudaGetLastError());
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+extern "C" int pdg_triplets_to_vector(const uint64_t* keys, const double* vals, int64_t n, int64_t n_rows,
+                                      double* out, void* workspace, size_t workspace_bytes, pdg_stream stream) {
+  PDG_TRY {
+    if (!keys || !vals || !out || !workspace) return fail(PDG_ERR_INVALID, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    PDG_CUDA(cudaMemsetAsync(out, 0, (size_t)std::max<int64_t>(n_rows, 0) * 8, st));
+    if (n <= 0 || n_rows <= 0) return PDG_OK;
+    const uint64_t lim = (uint64_t)n_rows;
+    Ws w;
+    uint64_t* ks;
+    double* vs;
+    int rc = sort_reduce(keys, vals, n, lim, workspace, workspace_bytes, st, w, &ks, &vs);
+    if (rc) return rc;
+    uint64_t* ukeys = ks == w.ukeys ? w.keys_alt : w.ukeys;
+    double* usums = vs == w.usums ? w.vals_alt : w.usums;
+    size_t tb = w.temp_bytes;
+    PDG_CUDA(cub::DeviceReduce::ReduceByKey(w.temp, tb, ks, ukeys, vs, usums, w.nruns, cub::Sum(), n, st));
+    note_launch();
+    scatter_vector<<<grid_for(n_rows, 256), 256, 0, st>>>(ukeys, usums, w.nruns, lim, out, n_rows);
+    note_launch();
+    PDG_CUDA(cudaGetLastError());
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
