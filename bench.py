@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--degree", type=int, default=None, help="override the workload degree")
     ap.add_argument("--n", type=int, default=None, help="override the workload size")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--approach", type=int, default=2, choices=(1, 2),
+                    help="2 = preset sparsity (default); 1 = stage-and-sort (triplets + device sort)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -313,6 +315,13 @@ def run_ours(args, w, rank, world, local_rank):
     if slab_case:
         plan = SlabPlan(slab, coeffs, specs, initial, cfg, row_elements=rows, device=dev, stream=stream)
         work = slab_work(plan)
+    elif args.approach == 1:
+        from paper_2007_04881_b200.approach1 import Approach1Plan
+
+        if world > 1:
+            raise NotImplementedError("Approach 1 bench runs on one GPU")
+        plan = Approach1Plan(pm, coeffs, specs, cfg, device=dev, stream=stream)
+        work = assembly_work(plan.base)
     else:
         plan = SipgPlan(pm, coeffs, specs, cfg, row_elements=rows, device=dev, stream=stream)
         work = assembly_work(plan)
@@ -344,6 +353,8 @@ def run_ours(args, w, rank, world, local_rank):
     ms_index = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     ms_pre = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     ms_el = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    if args.approach == 1 and not slab_case:  # events: start | pre-pass | emit | sort + merge
+        ms_pre, ms_el, ms_index = ms_index, ms_pre, ms_el
     plan.check_flags()
 
     # end to end through the plan API with host buffers
@@ -408,10 +419,12 @@ def run_ours(args, w, rank, world, local_rank):
                    if plan.nnz * 16 > 4e8 else "small workload: L2-resident",
                    "mesh_build_s": round(mesh_s, 1)},
         "phases_ms": {"index": ms_index, "prepass": ms_pre, "element_kernel": ms_el},
+        "approach": args.approach if not slab_case else 2,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(w.name, n_el),
                      "kernel": "pdg_slab_kernel (fused prism volume+lateral+bottom, DMMA f64)" if slab_case
-                     else "assemble_elements (fused volume+face+boundary, DMMA f64)",
+                     else ("pdg_a1_kernel (Approach 1 item emission, DMMA f64)" if args.approach == 1
+                           else "assemble_elements (fused volume+face+boundary, DMMA f64)"),
                      "algorithmic_flops_per_launch": work["flops"],
                      "algorithmic_bytes_per_launch": work["bytes"],
                      "hbm_achieved_gbs": gbs, "hbm_peak_gbs": hbm, "hbm_frac": gbs / hbm,

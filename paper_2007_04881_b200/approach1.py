@@ -125,15 +125,19 @@ class Approach1Plan:
         self.items = it
         self.stream = b.stream
 
-    def _emit(self):
+    def _prepass(self):
         b = self.base
         s = _lib.stream_ptr(self.stream)
-        self.t["keys"].fill_(-1)  # sentinel stripes (assembly.py:158-174)
         _lib.check(b.lib.pdg_frames_build(C.byref(b.dm.struct), C.byref(b.basis), C.byref(b.frames),
                                           _lib.ptr(b.t["flags"]), s))
         _lib.check(b.lib.pdg_face_prepass(C.byref(b.dm.struct), C.byref(b.basis), C.byref(b.coeffs),
                                           C.byref(b.rules.struct), C.byref(b.params), _lib.ptr(b.t["sigma"]),
                                           _lib.ptr(b.t["flow"]), _lib.ptr(b.t["abar"]), _lib.ptr(b.t["flags"]), s))
+
+    def _emit(self):
+        b = self.base
+        s = _lib.stream_ptr(self.stream)
+        self.t["keys"].fill_(-1)  # sentinel stripes (assembly.py:158-174)
         _lib.check(b.lib.pdg_a1_emit(C.byref(b.dm.struct), C.byref(b.basis), C.byref(b.coeffs), b.jit_source,
                                      C.byref(b.rules.struct), C.byref(b.params), C.byref(b.frames),
                                      _lib.ptr(b.t["sigma"]), _lib.ptr(b.t["flow"]), C.byref(self.items),
@@ -152,17 +156,22 @@ class Approach1Plan:
                                                 n, _lib.ptr(self.t["rhs"]), _lib.ptr(self.t["ws"]), self.ws_bytes, s))
 
     def run(self, events=None):
-        """Enqueue emission (kernels) then sort + merge (index phase); no host sync."""
+        """Enqueue frames + face pre-pass, item emission (the kernels), then
+        sort + merge (the index phase); no host sync.  ``events``: 4 CUDA
+        events recorded at the phase boundaries."""
         torch = _torch()
         with torch.cuda.stream(self.stream):
             if events:
                 events[0].record(self.stream)
-            self._emit()
+            self._prepass()
             if events:
                 events[1].record(self.stream)
-            self._merge()
+            self._emit()
             if events:
                 events[2].record(self.stream)
+            self._merge()
+            if events:
+                events[3].record(self.stream)
 
     def check_flags(self):
         self.base.check_flags()
@@ -177,6 +186,31 @@ class Approach1Plan:
     def rhs(self):
         return self.t["rhs"][: self.base.dof.n_dofs]
 
+    # HostIO / bench view (the CSR as produced by the merge)
+    @property
+    def dm(self):
+        return self.base.dm
+
+    @property
+    def dof(self):
+        return self.base.dof
+
+    @property
+    def nnz(self) -> int:
+        return self.base.nnz  # the merged pattern equals the preset one (tests/test_approach1.py)
+
+    @property
+    def row_ptr(self):
+        return self.t["row_ptr"][: self.base.dof.n_dofs + 1]
+
+    @property
+    def col_idx(self):
+        return self.t["col_idx"][: self.base.nnz]
+
+    @property
+    def values(self):
+        return self.t["values"][: self.base.nnz]
+
 
 def assemble_approach1_device(mesh, coeffs, specs, config: Optional[AssemblyConfig] = None):
     """Stage-and-sort assembly on the B200 (polydg ``assemble_approach1``,
@@ -185,10 +219,10 @@ def assemble_approach1_device(mesh, coeffs, specs, config: Optional[AssemblyConf
     t0 = time.perf_counter()
     _check_classified(mesh)
     plan = Approach1Plan(mesh, coeffs, specs, config)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     plan.run(ev)
     plan.check_flags()
-    ms_k, ms_idx = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+    ms_k, ms_idx = ev[0].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
     matrix = plan.to_csr()
     rhs = plan.rhs.cpu().numpy().copy()
     kern = plan.base.work_stats()
