@@ -379,6 +379,43 @@ int pdg_triplets_to_csr(const uint64_t* keys, const double* vals, int64_t n_trip
 int pdg_triplets_to_vector(const uint64_t* keys, const double* vals, int64_t n, int64_t n_rows,
                            double* out, void* workspace, size_t workspace_bytes, pdg_stream stream);
 
+/* ---- mesh preprocessing: agglomeration (polydg mesh.py:328-473) ----
+ * Simplicial mesh + element map -> the polytopic mesh arrays of pdg_mesh
+ * (same element / face / facet / interface order and conventions, bit for
+ * bit).  Caller-allocated device outputs with capacities: elem_ptr [nel+1],
+ * elem_simplices [ns], boxes [nel][2][dim], elem_volumes [nel]; every
+ * face / facet array [ns*(dim+1)] (+1 for face_ptr), interface arrays
+ * [ns*(dim+1)] (+1 for iface_ptr), elem_bface_ptr [nel+1].  The call
+ * synchronises the stream (output sizes are data dependent) and fills the
+ * counts.  iface_faces = 0..n_interior_faces-1, elem_bfaces = the rest. */
+typedef struct pdg_agg_out {
+  int64_t* elem_ptr;
+  int32_t* elem_simplices;
+  double* boxes;
+  double* elem_volumes;
+  int32_t* face_owner;
+  int32_t* face_neighbor;
+  double* face_normal;
+  double* face_measure;
+  int64_t* face_ptr;
+  int32_t* facet_vertices;
+  int32_t* facet_owner_simplex;
+  int32_t* facet_neighbor_simplex;
+  double* facet_measures;
+  int32_t* iface_owner;
+  int32_t* iface_neighbor;
+  int64_t* iface_ptr;
+  int64_t* elem_bface_ptr;
+  int64_t n_faces, n_facets, n_interfaces, n_interior_faces; /* outputs */
+} pdg_agg_out;
+
+size_t pdg_agglomerate_workspace_bytes(int32_t dim, int64_t n_simplices, int64_t n_elements);
+
+int pdg_agglomerate(int32_t dim, int64_t n_vertices, int64_t n_simplices, const double* vertices,
+                    const int32_t* simplices, const double* simplex_volumes, const int64_t* agg,
+                    int64_t n_elements, int32_t check_connected, pdg_agg_out* out, void* workspace,
+                    size_t workspace_bytes, pdg_stream stream);
+
 /* ---- unit-level entry points (tests / debugging) ---- */
 
 /* Mapped volume quadrature of simplices (quadrature.py:118-136):

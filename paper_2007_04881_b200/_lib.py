@@ -101,6 +101,14 @@ class A1Items(C.Structure):
                 ("load_offset", _p)]
 
 
+class AggOut(C.Structure):
+    _fields_ = [(n, _p) for n in ("elem_ptr", "elem_simplices", "boxes", "elem_volumes", "face_owner",
+                                  "face_neighbor", "face_normal", "face_measure", "face_ptr", "facet_vertices",
+                                  "facet_owner_simplex", "facet_neighbor_simplex", "facet_measures",
+                                  "iface_owner", "iface_neighbor", "iface_ptr", "elem_bface_ptr")] + \
+               [("n_faces", _i64), ("n_facets", _i64), ("n_interfaces", _i64), ("n_interior_faces", _i64)]
+
+
 SLAB_MAX_DEGREE = {"P": 5, "PQ": 4}  # include/pdg.h PDG_SLAB_MAX_DEGREE(_PQ)
 
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
@@ -109,6 +117,7 @@ EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspa
            "pdg_assemble", "pdg_assemble_jit", "pdg_jit_prepare",
            "pdg_slab_prepare", "pdg_slab_prepass", "pdg_slab_assemble",
            "pdg_a1_emit", "pdg_triplets_workspace_bytes", "pdg_triplets_to_csr", "pdg_triplets_to_vector",
+           "pdg_agglomerate_workspace_bytes", "pdg_agglomerate",
            "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks")
 
 
@@ -154,13 +163,16 @@ def load():
     lib.pdg_triplets_workspace_bytes.argtypes = [_i64]
     lib.pdg_triplets_to_csr.argtypes = [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, C.c_size_t, _p]
     lib.pdg_triplets_to_vector.argtypes = [_p, _p, _i64, _i64, _p, _p, C.c_size_t, _p]
+    lib.pdg_agglomerate_workspace_bytes.restype = C.c_size_t
+    lib.pdg_agglomerate_workspace_bytes.argtypes = [_i32, _i64, _i64]
+    lib.pdg_agglomerate.argtypes = [_i32, _i64, _i64, _p, _p, _p, _p, _i64, _i32, P(AggOut), _p, C.c_size_t, _p]
     lib.pdg_map_simplices.argtypes = [P(Mesh), P(Rules), _i32, _p, _i64, _p, _p, _p, _p]
     lib.pdg_tabulate.argtypes = [P(Mesh), P(Basis), _i32, _p, _i64, _p, _p, _p]
     lib.pdg_element_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params),
                                        P(Frames), _p, _i64, _p, _p, _p, _p]
     for name in EXPORTS:
         if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes",
-                        "pdg_triplets_workspace_bytes"):
+                        "pdg_triplets_workspace_bytes", "pdg_agglomerate_workspace_bytes"):
             getattr(lib, name).restype = C.c_int
     if lib.pdg_abi_version() != ABI_VERSION:
         raise EngineUnavailable("libpdg.so ABI version mismatch")

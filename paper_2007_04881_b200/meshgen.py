@@ -115,8 +115,14 @@ def voronoi_simplicial(n: int, seed: int = 0):
     return SimplicialMesh(2, verts, tris), agg
 
 
-def voronoi_mesh(n: int, seed: int = 0) -> PolytopicMesh:
+def voronoi_mesh(n: int, seed: int = 0, device: bool = False) -> PolytopicMesh:
+    """``device``: agglomerate on the GPU (meshprep.agglomerate_device, the
+    same mesh bit for bit) -- used for the million-cell benchmark meshes."""
     base, agg = voronoi_simplicial(n, seed)
+    if device:
+        from .meshprep import agglomerate_device
+
+        return agglomerate_device(base, agg, check_connected=False)
     return agglomerate(base, agg, check_connected=False)
 
 

@@ -96,7 +96,13 @@ def build_mesh(w: Workload) -> PolytopicMesh:
     from .meshgen import kuhn_agglomerated_mesh, voronoi_mesh
 
     if w.dim == 2:
-        return voronoi_mesh(w.n, seed=w.seed)
+        try:
+            import torch
+
+            on_gpu = torch.cuda.is_available() and w.n >= 100_000
+        except Exception:
+            on_gpu = False
+        return voronoi_mesh(w.n, seed=w.seed, device=on_gpu)
     return kuhn_agglomerated_mesh(w.n, w.k, seed=w.seed)
 
 
