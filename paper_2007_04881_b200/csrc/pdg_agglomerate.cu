@@ -5,8 +5,8 @@
 // conventions as polydg (and as this package's vectorised numpy
 // agglomerate, mesh.py), bit for bit:
 //   1. elements: stable sort of the simplices by element id (elem_ptr,
-//      elem_simplices ascending), boxes (min / max), volumes (numpy's
-//      pairwise summation order, so the floats match);
+//      elem_simplices ascending), boxes (min / max), volumes (np.add.reduceat's
+//      order -- first + pairwise sum of the rest -- so the floats match);
 //   2. facets: facet k of simplex s omits local vertex k (row s*(d+1)+k);
 //      sorted vertex ids -> 64-bit key; stable radix sort; equal keys pair
 //      two simplices (more than two: non-manifold); a pair inside one
@@ -118,7 +118,8 @@ __global__ void elem_geometry(const double* verts, const int32_t* simp, const do
       boxes[e * 2 * D + k] = lo[k];
       boxes[e * 2 * D + D + k] = hi[k];
     }
-    vols[e] = np_sum(svol, order + a, b - a);
+    // np.add.reduceat over a segment = first + pairwise sum of the rest
+    vols[e] = b - a > 1 ? svol[order[a]] + np_sum(svol, order + a + 1, b - a - 1) : svol[order[a]];
   }
 }
 
