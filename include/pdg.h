@@ -416,6 +416,25 @@ int pdg_agglomerate(int32_t dim, int64_t n_vertices, int64_t n_simplices, const 
                     int64_t n_elements, int32_t check_connected, pdg_agg_out* out, void* workspace,
                     size_t workspace_bytes, pdg_stream stream);
 
+/* ---- consumers of the device CSR (polydg solver.py:30-118) ----
+ * The element-block structure of the assembled CSR (every row of element e
+ * holds the same column list) is exploited: the column list is read once
+ * per element.  err_flags bits: 1 = an element row longer than 1024 columns
+ * (SpMV staging), 2 = missing diagonal block, 4 = singular diagonal block. */
+int pdg_spmv_blocked(const int64_t* dof_offset, int64_t n_elements, const int64_t* row_ptr,
+                     const int64_t* col_idx, const double* values, const double* x, double* y,
+                     uint32_t* err_flags, pdg_stream stream);
+
+/* Inverses of the element diagonal blocks (inverses[inv_offset[e] ...] row-major n_e x n_e). */
+int pdg_block_jacobi_setup(const int64_t* dof_offset, int64_t n_elements, int32_t max_block,
+                           const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                           const int64_t* inv_offset, double* inverses, uint32_t* err_flags,
+                           pdg_stream stream);
+
+/* z = blockdiag(inverses) r. */
+int pdg_block_jacobi_apply(const int64_t* dof_offset, int64_t n_elements, const int64_t* inv_offset,
+                           const double* inverses, const double* r, double* z, pdg_stream stream);
+
 /* ---- unit-level entry points (tests / debugging) ---- */
 
 /* Mapped volume quadrature of simplices (quadrature.py:118-136):

@@ -118,6 +118,7 @@ EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspa
            "pdg_slab_prepare", "pdg_slab_prepass", "pdg_slab_assemble",
            "pdg_a1_emit", "pdg_triplets_workspace_bytes", "pdg_triplets_to_csr", "pdg_triplets_to_vector",
            "pdg_agglomerate_workspace_bytes", "pdg_agglomerate",
+           "pdg_spmv_blocked", "pdg_block_jacobi_setup", "pdg_block_jacobi_apply",
            "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks")
 
 
@@ -166,6 +167,9 @@ def load():
     lib.pdg_agglomerate_workspace_bytes.restype = C.c_size_t
     lib.pdg_agglomerate_workspace_bytes.argtypes = [_i32, _i64, _i64]
     lib.pdg_agglomerate.argtypes = [_i32, _i64, _i64, _p, _p, _p, _p, _i64, _i32, P(AggOut), _p, C.c_size_t, _p]
+    lib.pdg_spmv_blocked.argtypes = [_p, _i64, _p, _p, _p, _p, _p, _p, _p]
+    lib.pdg_block_jacobi_setup.argtypes = [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p]
+    lib.pdg_block_jacobi_apply.argtypes = [_p, _i64, _p, _p, _p, _p, _p]
     lib.pdg_map_simplices.argtypes = [P(Mesh), P(Rules), _i32, _p, _i64, _p, _p, _p, _p]
     lib.pdg_tabulate.argtypes = [P(Mesh), P(Basis), _i32, _p, _i64, _p, _p, _p]
     lib.pdg_element_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params),

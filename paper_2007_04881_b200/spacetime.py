@@ -506,11 +506,14 @@ def assemble_slab(slab, coeffs, specs, u_prev, config=None, approach=2, dirichle
 
 
 def _default_solver(matrix, rhs, dof_map):
-    """Sparse direct solve on the host (polydg's default is block-Jacobi GMRES,
-    solver.py:74-118 -- a consumer of the assembly, out of this engine's scope)."""
-    from scipy.sparse.linalg import spsolve
+    """polydg's default (spacetime.py:448-456): block-Jacobi preconditioned
+    GMRES -- here on the device (solver.py)."""
+    from .solver import solve
 
-    return spsolve(matrix.to_scipy().tocsc(), rhs)
+    result = solve(matrix, rhs, dof_map=dof_map)
+    if not result.converged:
+        raise RuntimeError(f"linear solve stagnated (residual {result.residual:.3e})")
+    return result.x
 
 
 def march(spatial_mesh, time_partition, problem, degrees, family=Family.PQ, config=None, solver=None,
