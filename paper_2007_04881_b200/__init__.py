@@ -59,5 +59,18 @@ from .distribute import (
     quadrature_cost_weights,
 )
 
+from .spacetime import (
+    ParabolicProblem,
+    SlabMesh,
+    SlabPlan,
+    TimePartition,
+    assemble_slab,
+    build_slab,
+    load_solution_vector,
+    march,
+    save_solution_vector,
+)
+from .solver import SolveResult, SolverError, read_matrix_market, solve, write_matrix_market
+
 __all__ = [n for n in dir() if not n.startswith("_")]
 __version__ = "0.1.0"

@@ -24,9 +24,14 @@ def test_matrix_market_roundtrip(tmp_path):
 
 
 def _system(coeff="poisson_sine", p=2):
+    from paper_2007_04881_b200.mesh import agglomerate
     from paper_2007_04881_b200.meshgen import voronoi_mesh
 
-    pm = voronoi_mesh(150, seed=1)
+    if coeff == "generic":  # b = (1 + x, 1) straddles some Voronoi faces: the grid clusters of the golden set
+        g = F.square_grid(10)
+        pm = agglomerate(g, F.grown_clusters(g, 23, seed=2))
+    else:
+        pm = voronoi_mesh(150, seed=1)
     C = getattr(F, coeff)(2)
     classify_boundary_faces(pm, C)
     specs = build_basis(pm, p)
