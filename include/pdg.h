@@ -180,7 +180,8 @@ typedef struct pdg_iface_rec {
   double sig;       /* penalty of face fa (model.py:238-257) */
   double nrm[3];    /* owner normal of face fa */
   int64_t dof;      /* first global DoF of j (= first column index of its block) */
-  int64_t pad_;
+  int32_t nrows0;   /* sub-facet rows of face fa */
+  int32_t pad_;
 } pdg_iface_rec;
 
 /* Block pattern of the rows owned by one assembly (assembly.py:209-340). */

@@ -271,6 +271,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   // async-copied geometry: the element's simplex frames, the window's first facet frames
   double* sfr = rhs_s + (S::RHS_REGS ? 0 : 32 * NB);
   double* ffr = sfr + FR_MAX * W::SF;
+  // basis constants (element records) of the window's neighbours
+  double* ebx = ffr + NBR_WIN * W::FF;
 
   const int kv = KV ? KV : a.lay.kv, kvp = kv + 4;
   const int dk = cf.diff_kind();
@@ -309,11 +311,16 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
     return true;
   };
   // first facet frame of every non-self interface of a staged window -> ffr[entry]
+  // and the neighbour's basis constants -> ebx[entry] (no dependent global
+  // loads left on the first face of an interface)
   auto issue_ffr = [&](const pdg_iface_rec* rw, int nw, int32_t e) {
     if (lane < nw && rw[lane].j != e) {
       const double* src = a.fframe + (int64_t)rw[lane].row0 * W::FF;
 #pragma unroll
       for (int c = 0; c < W::FF / 2; ++c) cp_async16(ffr + lane * W::FF + 2 * c, src + 2 * c);
+      const double* bsrc = a.erec + (int64_t)rw[lane].j * W::ER;
+#pragma unroll
+      for (int c = 0; c < W::ER / 2; ++c) cp_async16(ebx + lane * W::ER + 2 * c, bsrc + 2 * c);
     }
   };
   int rb = 0;
@@ -662,7 +669,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           double nrm[3] = {0.0, 0.0, 0.0};
 #pragma unroll
           for (int i = 0; i < DIM; ++i) nrm[i] = rc[q].nrm[i];
-          const BoxConst<DIM> bo = load_box<DIM>(a.erec, rc[q].j);
+          const BoxConst<DIM> bo = load_box<DIM>(ebx, q);
           tab_slot(nrm, ffr + q * W::FF, r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, rc[q].sig,
                    (info & 1) ? -1.0 : 1.0, (info & 2) != 0, bo);
           __syncwarp();
@@ -678,9 +685,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           continue;
         }
         // ---- general interface: every face, every sub-facet, rounds of 16 points
-        const int32_t j = rc[qi].j;
         const int pj = rc[qi].pj;
-        const BoxConst<DIM> bo = load_box<DIM>(a.erec, j);
+        const BoxConst<DIM> bo = load_box<DIM>(ebx, qi);
         const int order = 2 * max(pe, pj) + a.prm.quad_increment;
         const int r0 = R.face_offset[order], nq = R.face_count[order];
         const int fend = rc[qi].fb;
@@ -697,6 +703,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 #pragma unroll
             for (int i = 0; i < DIM; ++i) nrm[i] = rc[qi].nrm[i];
             row0 = rc[qi].row0;
+            nrows = rc[qi].nrows0;
           } else {
             side = m.face_owner[f] == e ? 0 : 1;
             info = side | ((cf.has_adv() && a.flow[f] == side) ? 2 : 0);
@@ -704,15 +711,18 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 #pragma unroll
             for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)f * DIM + i];
             row0 = m.face_ptr[f];
+            nrows = (int)(m.face_ptr[f + 1] - row0);
           }
-          nrows = (int)(m.face_ptr[f + 1] - row0);
+          const bool first_face = f == rc[qi].fa;
           const int Pf = nrows * nq;
           for (int base = 0; base < Pf; base += KF) {
             const int nvalid = min(KF, Pf - base);
             const int gq = base + min(slot, nvalid - 1);
             const int lr = gq / nq;
-            tab_slot(nrm, a.fframe + (row0 + lr) * W::FF, r0, gq - lr * nq, slot < nvalid ? 1.0 : 0.0, sig,
-                     side ? -1.0 : 1.0, (info & 2) != 0, bo);
+            // the first sub-facet frame of the interface is staged (ffr)
+            const double* frp = (first_face && lr == 0) ? ffr + qi * W::FF : a.fframe + (row0 + lr) * W::FF;
+            tab_slot(nrm, frp, r0, gq - lr * nq, slot < nvalid ? 1.0 : 0.0, sig, side ? -1.0 : 1.0,
+                     (info & 2) != 0, bo);
             __syncwarp();
             face_contract(0, (nvalid + 3) >> 2, co);
             __syncwarp();

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, co
     for (int64_t c0 = q0; c0 < q1; c0 += 32) {
       const int nv = (int)(q1 - c0 < 32 ? q1 - c0 : 32);
       const int64_t q = c0 + lane;
-      int j = 0, nj = 0, pj = 0, fa = 0, fb = 0, row0 = 0, info = 0;
+      int j = 0, nj = 0, pj = 0, fa = 0, fb = 0, row0 = 0, info = 0, nrows = 0;
       double sig = 0.0, nrm[3] = {0.0, 0.0, 0.0};
       long long dof = 0;
       if (lane < nv) {
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, co
           const int side = m.face_owner[fa] == e ? 0 : 1;
           const bool down = has_adv && flow[fa] == side;
           row0 = (int)m.face_ptr[fa];
-          const int nrows = (int)(m.face_ptr[fa + 1] - row0);
+          nrows = (int)(m.face_ptr[fa + 1] - row0);
           const int nq = R.face_count[2 * max(pe, pj) + inc];
           const bool simple = fb - fa == 1 && nrows == 1 && nq <= 8;
           info = side | (down ? 2 : 0) | (simple ? 4 : 0);
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, co
         double2* rd = reinterpret_cast<double2*>(r + 2);
         rd[0] = make_double2(sig, nrm[0]);
         rd[1] = make_double2(nrm[1], nrm[2]);
-        reinterpret_cast<longlong2*>(r + 4)[0] = make_longlong2(dof, 0);
+        reinterpret_cast<longlong2*>(r + 4)[0] = make_longlong2(dof, (long long)(unsigned)nrows);
       }
       __syncwarp();
       int4* dst = reinterpret_cast<int4*>(P.nbr_rec + c0);
