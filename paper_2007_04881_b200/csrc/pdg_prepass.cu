@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, co
         double2* rd = reinterpret_cast<double2*>(r + 2);
         rd[0] = make_double2(sig, nrm[0]);
         rd[1] = make_double2(nrm[1], nrm[2]);
-        reinterpret_cast<longlong2*>(r + 4)[0] = make_longlong2(dof, (long long)(unsigned)nrows);
+        // first-face row count: read by the 3D element kernel only
+        reinterpret_cast<longlong2*>(r + 4)[0] = make_longlong2(dof, DIM == 3 ? (long long)(unsigned)nrows : 0ll);
       }
       __syncwarp();
       int4* dst = reinterpret_cast<int4*>(P.nbr_rec + c0);
