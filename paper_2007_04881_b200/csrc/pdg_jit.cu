@@ -141,10 +141,13 @@ static bool jit_ws() {
 
 // PDG_JIT_WARPS: warps per CTA of the single-warp body (default 4).  Small CTAs
 // let the register budget, not the CTA granularity, set the resident warp count.
-static int jit_warps() {
+// Default by dimension (measured r01, same box, cfg4 3D p=2: 4 warps x 3 CTAs
+// 10.25 ms, 2 x 6 9.89 ms, 1 x 12 10.38 ms; 2D keeps 4 x 3).
+static int jit_warps(int dim) {
   const char* v = getenv("PDG_JIT_WARPS");
-  const int w = v ? atoi(v) : 4;
-  return w >= 1 && w <= 8 ? w : 4;
+  const int def = dim == 3 ? 2 : 4;
+  const int w = v ? atoi(v) : def;
+  return w >= 1 && w <= 8 ? w : def;
 }
 
 static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv) {
@@ -154,7 +157,7 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
   // warp-specialised body: CTA = 64 threads (one pair), default 8 (128 registers)
   const bool ws = jit_ws();
   const char* mb = getenv("PDG_JIT_MINBLOCKS");
-  const int minblocks = mb ? std::max(1, atoi(mb)) : (ws ? 8 : 3);
+  const int minblocks = mb ? std::max(1, atoi(mb)) : (ws ? 8 : 12 / jit_warps(dim));
   std::ostringstream os;
   os << "#include \"" << (ws ? "assemble_ws.cuh" : "assemble_body.cuh") << "\"\n"
      << "namespace pdg_jit {\nusing namespace pdg;\n"
@@ -164,7 +167,7 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
   if (const char* mr = getenv("PDG_JIT_MAXNREG"))
     os << "__maxnreg__(" << atoi(mr) << ")";
   else
-    os << "__launch_bounds__(" << (ws ? 64 : 32 * jit_warps()) << ", " << minblocks << ")";
+    os << "__launch_bounds__(" << (ws ? 64 : 32 * jit_warps(dim)) << ", " << minblocks << ")";
   os << " pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {\n"
      << "  pdg::" << (ws ? "assemble_ws<" : "assemble_body<") << dim << ", " << P << ", "
      << (sym ? "true" : "false");
@@ -321,7 +324,7 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     a.lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, jit_rhs_regs_max());
     const std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, sym, a.lay.kv, k);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
-    int threads = 32 * jit_warps();
+    int threads = 32 * jit_warps(mesh->dim);
     // the CTA's rule copy (always reserved: the JIT build may toggle PDG_RULES_SMEM)
     size_t smem = ((size_t)rule_smem_doubles(rules->n_points) + (size_t)a.lay.warp_doubles * (threads / 32)) * 8;
     if (ws) {  // one producer/consumer pair per CTA: two stages + header + neighbour staging
