@@ -479,6 +479,7 @@ extern "C" int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, c
     if (!pattern->nbr_ptr || !pattern->nbr_elem || !pattern->nbr_iface || !pattern->row_len ||
         !pattern->elem_val_offset)
       return fail(PDG_ERR_INVALID, "pattern not built (pdg_adjacency / pdg_pattern_offsets)");
+    if (!pattern->nbr_rec) return fail(PDG_ERR_INVALID, "interface records missing (pdg_iface_records)");
     if (pattern->n_row_elements <= 0) return PDG_OK;
     const int P = basis->max_degree, fam = slab->family, nw = slab_warps(P, fam);
     CUmod mod = nullptr;

@@ -34,7 +34,7 @@ namespace pdg {
 
 constexpr int SLAB_KS = 32;       // quadrature slots per round (lane = slot)
 constexpr int SLAB_KSP = 36;      // slot stride (4 mod 16 doubles: conflict-free fragment loads)
-constexpr int SLAB_NBR_MAX = 64;  // neighbours per element staged in shared memory
+constexpr int SLAB_NBR_MAX = 32;  // neighbours per element staged in shared memory (occupancy: keep small)
 constexpr int SLAB_NSC = 8;       // per-slot scalar rows
 
 template <int N>
@@ -137,8 +137,9 @@ inline __host__ __device__ int slab_table_doubles(int rows, int nbp, int nt, int
   return t > red ? t : red;
 }
 inline __host__ __device__ size_t slab_smem_bytes(int rows, int nbp, int nt, int nw) {
-  return ((size_t)slab_table_doubles(rows, nbp, nt, nw) + SLAB_NSC * SLAB_KS + nbp) * 8 +
-         (size_t)SLAB_NBR_MAX * 4 * sizeof(int32_t);
+  // table, per-slot scalars, RHS, neighbour staging (3 doubles + 8 ints per entry)
+  return ((size_t)slab_table_doubles(rows, nbp, nt, nw) + SLAB_NSC * SLAB_KS + nbp + 3 * SLAB_NBR_MAX) * 8 +
+         (size_t)SLAB_NBR_MAX * 8 * sizeof(int32_t);
 }
 
 template <class CF>
@@ -273,10 +274,19 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
   }
   double* sc = smem + slab_table_doubles(a.sl.table_rows, NBP, NT, NW);  // [SLAB_NSC][32]
   double* rhs_s = sc + SLAB_NSC * SLAB_KS;                     // [NBP]
-  int32_t* nb_j = reinterpret_cast<int32_t*>(rhs_s + NBP);     // [SLAB_NBR_MAX] x 4
-  int32_t* nb_if = nb_j + SLAB_NBR_MAX;
-  int32_t* nb_col = nb_if + SLAB_NBR_MAX;
+  // neighbour window staged from the interface records (pdg_iface_rec,
+  // pdg_prepass.cu): no dependent global loads before a face point
+  double* nb_sig = rhs_s + NBP;                                   // [SLAB_NBR_MAX]
+  double* nb_n0 = nb_sig + SLAB_NBR_MAX;
+  double* nb_n1 = nb_n0 + SLAB_NBR_MAX;
+  int32_t* nb_j = reinterpret_cast<int32_t*>(nb_n1 + SLAB_NBR_MAX);
+  int32_t* nb_col = nb_j + SLAB_NBR_MAX;
   int32_t* nb_n = nb_col + SLAB_NBR_MAX;
+  int32_t* nb_pj = nb_n + SLAB_NBR_MAX;
+  int32_t* nb_fa = nb_pj + SLAB_NBR_MAX;
+  int32_t* nb_fb = nb_fa + SLAB_NBR_MAX;
+  int32_t* nb_info = nb_fb + SLAB_NBR_MAX;
+  int32_t* nb_row0 = nb_info + SLAB_NBR_MAX;
   auto TAB = [&](int row, int f, int slot) -> double& { return T[(row * NBP + f) * KSP + slot]; };
   double* const s0_ = sc;             // volume: w a_00 (diag) / w (full) | face: alpha
   double* const s1_ = sc + 32;        // w a_11 | beta
@@ -302,18 +312,20 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
     const int64_t Lrow = pat.row_len[k];
     const int64_t q0 = pat.nbr_ptr[e];
     const int nnb = (int)(pat.nbr_ptr[e + 1] - q0);
-    if (threadIdx.x == 0) {
-      if (nnb > SLAB_NBR_MAX) raise_flag(a.flags, PDG_FLAG_STACK);
-      int col = 0;
-      for (int q = 0; q < min(nnb, SLAB_NBR_MAX); ++q) {
-        const int32_t j = pat.nbr_elem[q0 + q];
-        const int nj = (int)(B.dof_offset[j + 1] - B.dof_offset[j]);
-        nb_j[q] = j;
-        nb_if[q] = pat.nbr_iface[q0 + q];
-        nb_col[q] = col;
-        nb_n[q] = nj;
-        col += nj;
-      }
+    if (threadIdx.x == 0 && nnb > SLAB_NBR_MAX) raise_flag(a.flags, PDG_FLAG_STACK);
+    for (int q = threadIdx.x; q < min(nnb, SLAB_NBR_MAX); q += NW * 32) {
+      const pdg_iface_rec& rec = pat.nbr_rec[q0 + q];
+      nb_j[q] = rec.j;
+      nb_col[q] = rec.col;
+      nb_n[q] = rec.nj;
+      nb_pj[q] = rec.pj;
+      nb_fa[q] = rec.fa;
+      nb_fb[q] = rec.fb;
+      nb_info[q] = rec.info;
+      nb_row0[q] = rec.row0;
+      nb_sig[q] = rec.sig;
+      nb_n0[q] = rec.nrm[0];
+      nb_n1[q] = rec.nrm[1];
     }
     for (int f = threadIdx.x; f < NBP; f += NW * 32) rhs_s[f] = 0.0;
     __syncthreads();
@@ -542,22 +554,23 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
     for (int qn = 0; qn < min(nnb, SLAB_NBR_MAX); ++qn) {
       const int32_t j = nb_j[qn];
       if (j == e) continue;
-      const int ifc = nb_if[qn];
-      const int pj = B.degree[j];
+      const int pj = nb_pj[qn];
       const BoxConst<3> bo = slab_box(a.erec, j, tbox);
       const int order = 2 * max(pe, pj) + a.prm.quad_increment;
       const int r0e = R.face_offset[order], nqe = R.face_count[order];
       const int nqf = nqe * nqe;  // edge rule x time rule of the same order
       double co[TR][TC][2];
       slab_zero<TR, TC>(co);
-      for (int64_t fi = m.iface_ptr[ifc]; fi < m.iface_ptr[ifc + 1]; ++fi) {
-        const int32_t f = m.iface_faces[fi];
-        const int side = m.face_owner[f] == e ? 0 : 1;
+      for (int32_t f = nb_fa[qn]; f < nb_fb[qn]; ++f) {
+        // the interface's first face from the staged record, further faces from the mesh
+        const bool first = f == nb_fa[qn];
+        const int side = first ? (nb_info[qn] & 1) : (m.face_owner[f] == e ? 0 : 1);
         const double sgn = side ? -1.0 : 1.0;
-        const bool down = CF::has_adv() && a.flow[f] == side;
-        const double sig = a.sigma[f];
-        double nrm[3] = {m.face_normal[(int64_t)f * 2], m.face_normal[(int64_t)f * 2 + 1], 0.0};
-        const int64_t row0 = m.face_ptr[f];
+        const bool down = CF::has_adv() && (first ? (nb_info[qn] & 2) != 0 : a.flow[f] == side);
+        const double sig = first ? nb_sig[qn] : a.sigma[f];
+        double nrm[3] = {first ? nb_n0[qn] : m.face_normal[(int64_t)f * 2],
+                         first ? nb_n1[qn] : m.face_normal[(int64_t)f * 2 + 1], 0.0};
+        const int64_t row0 = first ? (int64_t)nb_row0[qn] : m.face_ptr[f];
         const int Pf = (int)(m.face_ptr[f + 1] - row0) * nqf;
         for (int base = 0; base < Pf; base += SLAB_KS) {
           const int nvalid = min(SLAB_KS, Pf - base);

@@ -306,6 +306,7 @@ class SlabPlan:
         self.t.update(nbr_ptr=z(nel + 1, i64), nbr_elem=z(nadj, i32), nbr_iface=z(nadj, i32),
                       row_len=z(nr, i64), val_off=z(nr + 1, i64), row_off=z(nr + 1, i64),
                       row_ptr=z(self.n_local_rows + 1, i64),
+                      nbr_rec=z(nadj * 10, torch.float64),  # pdg_iface_rec, 80 B per entry
                       sigma=z(flat.n_faces, torch.float64), flow=z(flat.n_faces, torch.int8),
                       flags=torch.zeros(1, dtype=torch.int32, device=dev),
                       sframe=z(flat.n_simplices * 8, torch.float64), fframe=z(flat.n_facets * 8, torch.float64),
@@ -323,7 +324,11 @@ class SlabPlan:
         pat.row_len, pat.elem_val_offset, pat.elem_row_offset = (
             _lib.ptr(self.t["row_len"]), _lib.ptr(self.t["val_off"]), _lib.ptr(self.t["row_off"]))
         pat.row_ptr = _lib.ptr(self.t["row_ptr"])
+        pat.nbr_rec = _lib.ptr(self.t["nbr_rec"])
         self.pattern = pat
+        # kind flags the interface-record pre-pass reads (advection -> downwind bit)
+        self.cflags = _lib.Coeffs()
+        self.cflags.has_advection = int(self.policy_info["adv"])
         with torch.cuda.stream(self.stream):
             self._index_phase(size_query=True)
         self.t["col_idx"] = z(self.nnz, i64)
@@ -358,6 +363,9 @@ class SlabPlan:
             C.byref(self.dm.struct), C.byref(self.basis), self.policy, C.byref(self.rules.struct),
             C.byref(self.params), C.byref(self.sdesc), C.byref(self.frames), _lib.ptr(self.t["sigma"]),
             _lib.ptr(self.t["flow"]), _lib.ptr(self.t["flags"]), s))
+        _lib.check(self.lib.pdg_iface_records(
+            C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.cflags), C.byref(self.rules.struct),
+            C.byref(self.params), C.byref(self.pattern), _lib.ptr(self.t["sigma"]), _lib.ptr(self.t["flow"]), s))
 
     def _elements(self):
         from . import _lib
@@ -393,7 +401,7 @@ class SlabPlan:
         self.stream.synchronize()
         flags = int(self.t["flags"].item())
         if flags & _lib.FLAG_STACK:
-            raise NotImplementedError("slab element with more than 64 neighbours (device staging capacity)")
+            raise NotImplementedError("slab element with more than 32 neighbours (device staging capacity)")
         _raise_flags(flags)
 
     # -- results ----------------------------------------------------------------
