@@ -314,6 +314,13 @@ int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coe
                      const int8_t* face_flow, double* values, int32_t write_col_idx, double* rhs,
                      uint32_t* err_flags, pdg_stream stream);
 
+/* pdg_face_prepass with the coefficient fields inlined (the NVRTC module of
+ * pdg_assemble_jit carries the pre-pass kernels). */
+int pdg_face_prepass_jit(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                         const char* policy_source, const pdg_rules* rules, const pdg_params* params,
+                         double* sigma, int8_t* face_flow, double* elem_abar, uint32_t* err_flags,
+                         pdg_stream stream);
+
 /* Compile (or fetch from the cache) the specialisation pdg_assemble_jit would
  * use; lets callers pay the NVRTC cost outside timed regions. */
 int pdg_jit_prepare(const pdg_coeffs* coeffs, const char* policy_source, int32_t dim,

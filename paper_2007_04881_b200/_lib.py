@@ -114,7 +114,7 @@ SLAB_MAX_DEGREE = {"P": 5, "PQ": 4}  # include/pdg.h PDG_SLAB_MAX_DEGREE(_PQ)
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
 EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes", "pdg_adjacency",
            "pdg_pattern_offsets", "pdg_pattern_fill", "pdg_face_prepass", "pdg_iface_records", "pdg_frames_build",
-           "pdg_assemble", "pdg_assemble_jit", "pdg_jit_prepare",
+           "pdg_assemble", "pdg_assemble_jit", "pdg_jit_prepare", "pdg_face_prepass_jit",
            "pdg_slab_prepare", "pdg_slab_prepass", "pdg_slab_assemble",
            "pdg_a1_emit", "pdg_triplets_workspace_bytes", "pdg_triplets_to_csr", "pdg_triplets_to_vector",
            "pdg_agglomerate_workspace_bytes", "pdg_agglomerate",
@@ -152,6 +152,8 @@ def load():
                                  P(Frames), _p, _p, _p, _i32, _p, _p, _p]
     lib.pdg_assemble_jit.argtypes = [P(Mesh), P(Basis), P(Coeffs), C.c_char_p, P(Rules), P(Params),
                                      P(Pattern), P(Frames), _p, _p, _p, _i32, _p, _p, _p]
+    lib.pdg_face_prepass_jit.argtypes = [P(Mesh), P(Basis), P(Coeffs), C.c_char_p, P(Rules), P(Params),
+                                         _p, _p, _p, _p, _p]
     lib.pdg_jit_prepare.argtypes = [P(Coeffs), C.c_char_p, _i32, _i32]
     lib.pdg_slab_prepare.argtypes = [C.c_char_p, _i32, _i32]
     lib.pdg_slab_prepass.argtypes = [P(Mesh), P(Basis), C.c_char_p, P(Rules), P(Params), P(Slab),

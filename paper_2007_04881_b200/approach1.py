@@ -126,13 +126,8 @@ class Approach1Plan:
         self.stream = b.stream
 
     def _prepass(self):
-        b = self.base
-        s = _lib.stream_ptr(self.stream)
-        _lib.check(b.lib.pdg_frames_build(C.byref(b.dm.struct), C.byref(b.basis), C.byref(b.frames),
-                                          _lib.ptr(b.t["flags"]), s))
-        _lib.check(b.lib.pdg_face_prepass(C.byref(b.dm.struct), C.byref(b.basis), C.byref(b.coeffs),
-                                          C.byref(b.rules.struct), C.byref(b.params), _lib.ptr(b.t["sigma"]),
-                                          _lib.ptr(b.t["flow"]), _lib.ptr(b.t["abar"]), _lib.ptr(b.t["flags"]), s))
+        self.base._frames()
+        self.base._face_prepass()
 
     def _emit(self):
         b = self.base

@@ -502,17 +502,31 @@ class SipgPlan:
         if size_query:
             self.nnz = int(nnz.value)
 
-    def _prepass(self):
+    def _frames(self):
         import ctypes as C
 
         _lib.check(self.lib.pdg_frames_build(C.byref(self.dm.struct), C.byref(self.basis),
                                              C.byref(self.frames), _lib.ptr(self.t["flags"]),
                                              _lib.stream_ptr(self.stream)))
-        _lib.check(self.lib.pdg_face_prepass(
-            C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs),
-            C.byref(self.rules.struct), C.byref(self.params), _lib.ptr(self.t["sigma"]),
-            _lib.ptr(self.t["flow"]), _lib.ptr(self.t["abar"]), _lib.ptr(self.t["flags"]),
-            _lib.stream_ptr(self.stream)))
+
+    def _face_prepass(self):
+        import ctypes as C
+
+        args = (C.byref(self.rules.struct), C.byref(self.params), _lib.ptr(self.t["sigma"]),
+                _lib.ptr(self.t["flow"]), _lib.ptr(self.t["abar"]), _lib.ptr(self.t["flags"]),
+                _lib.stream_ptr(self.stream))
+        if self.jit_source is not None:  # fields inlined (the NVRTC module of the element kernel)
+            _lib.check(self.lib.pdg_face_prepass_jit(C.byref(self.dm.struct), C.byref(self.basis),
+                                                     C.byref(self.coeffs), self.jit_source, *args))
+        else:
+            _lib.check(self.lib.pdg_face_prepass(C.byref(self.dm.struct), C.byref(self.basis),
+                                                 C.byref(self.coeffs), *args))
+
+    def _prepass(self):
+        import ctypes as C
+
+        self._frames()
+        self._face_prepass()
         _lib.check(self.lib.pdg_iface_records(
             C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs),
             C.byref(self.rules.struct), C.byref(self.params), C.byref(self.pattern),

@@ -153,26 +153,6 @@ struct NbrStage {
   int row0[NBR_WIN];       // first sub-facet row of the first face
 };
 
-// Ahead-of-time coefficient policy: interprets the bytecode in pdg_coeffs.
-template <int DIM>
-struct InterpCoef {
-  const pdg_coeffs& C;
-  __device__ InterpCoef(const pdg_coeffs& c) : C(c) {}
-  __device__ int diff_kind() const { return C.diffusion_kind; }
-  __device__ bool has_adv() const { return C.has_advection; }
-  __device__ bool has_reac() const { return C.has_reaction; }
-  __device__ bool has_src() const { return C.has_source; }
-  __device__ bool has_dir() const { return C.has_dirichlet; }
-  __device__ bool has_neu() const { return C.has_neumann; }
-  __device__ double a_iso(const double* x) const { return eval_prog(C, C.diffusion[0], x); }
-  __device__ double a_ij(int i, int j, const double* x) const { return eval_prog(C, C.diffusion[i * DIM + j], x); }
-  __device__ double b_i(int i, const double* x) const { return eval_prog(C, C.advection[i], x); }
-  __device__ double c(const double* x) const { return eval_prog(C, C.reaction, x); }
-  __device__ double f(const double* x) const { return eval_prog(C, C.source, x); }
-  __device__ double gD(const double* x) const { return eval_prog(C, C.dirichlet, x); }
-  __device__ double gN(const double* x) const { return eval_prog(C, C.neumann, x); }
-};
-
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }

@@ -160,6 +160,7 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
   const int minblocks = mb ? std::max(1, atoi(mb)) : (ws ? 8 : 12 / jit_warps(dim));
   std::ostringstream os;
   os << "#include \"" << (ws ? "assemble_ws.cuh" : "assemble_body.cuh") << "\"\n"
+     << "#include \"prepass_body.cuh\"\n"
      << "namespace pdg_jit {\nusing namespace pdg;\n"
      << policy << "\n}\n"
      << "extern \"C\" __global__ void ";
@@ -173,6 +174,14 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
      << (sym ? "true" : "false");
   if (!ws) os << ", pdg_jit::JitCoef, " << kv;
   os << ">(a, pdg_jit::JitCoef());\n}\n";
+  // the face pre-pass with the same inlined fields (pdg_face_prepass_jit)
+  os << "extern \"C\" __global__ void __launch_bounds__(256) pdg_jit_abar(const pdg_mesh m, const pdg_basis B, "
+        "const pdg_rules R, const pdg_params prm, double* abar, uint32_t* flags) {\n"
+     << "  pdg::elem_abar_body<" << dim << ">(m, B, pdg_jit::JitCoef(), R, prm, abar, flags);\n}\n"
+     << "extern \"C\" __global__ void __launch_bounds__(128) pdg_jit_face_prepass(const pdg_mesh m, "
+        "const pdg_basis B, const pdg_rules R, const pdg_params prm, const double* abar, double* sigma, "
+        "int8_t* flow, uint32_t* flags) {\n"
+     << "  pdg::face_prepass_body<" << dim << ">(m, B, pdg_jit::JitCoef(), R, prm, abar, sigma, flow, flags);\n}\n";
   return os.str();
 }
 
@@ -347,6 +356,50 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
                          nullptr) != 0)
       return fail(PDG_ERR_CUDA, "cuLaunchKernel failed");
     note_launch();
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+extern "C" int pdg_face_prepass_jit(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                                    const char* policy_source, const pdg_rules* rules, const pdg_params* params,
+                                    double* sigma, int8_t* face_flow, double* elem_abar, uint32_t* err_flags,
+                                    pdg_stream stream) {
+  PDG_TRY {
+    int rc = check_common(mesh, basis, coeffs);
+    if (rc) return rc;
+    if (!policy_source || !rules || !params || !sigma || !face_flow) return fail(PDG_ERR_INVALID, "null argument");
+    const bool iso_var = coeffs->diffusion_kind == PDG_DIFF_ISO && !coeffs->diffusion[0].is_const;
+    if (iso_var && !elem_abar) return fail(PDG_ERR_INVALID, "elem_abar scratch required");
+    // the module of the element kernel (same policy, dim, degree) carries the pre-pass kernels
+    const int kv = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind,
+                               coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max()).kv;
+    JitKernel k;
+    std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, symmetric_accumulation(*coeffs), kv, k);
+    CUfunc fa = nullptr, ff = nullptr;
+    if (err.empty()) err = get_function(k.mod, "pdg_jit_abar", fa);
+    if (err.empty()) err = get_function(k.mod, "pdg_jit_face_prepass", ff);
+    if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
+    pdg_mesh m = *mesh;
+    pdg_basis B = *basis;
+    pdg_rules R = *rules;
+    pdg_params prm = *params;
+    Api& A = api();
+    if (iso_var && mesh->n_elements > 0) {
+      void* args[] = {&m, &B, &R, &prm, &elem_abar, &err_flags};
+      if (A.cuLaunchKernel(fa, (unsigned)grid_for_warps(mesh->n_elements, 256), 1, 1, 256, 1, 1, 0,
+                           (cudaStream_t)stream, args, nullptr) != 0)
+        return fail(PDG_ERR_CUDA, "cuLaunchKernel(pdg_jit_abar) failed");
+      note_launch();
+    }
+    if (mesh->n_faces > 0) {
+      const double* ab = elem_abar;
+      void* args[] = {&m, &B, &R, &prm, &ab, &sigma, &face_flow, &err_flags};
+      if (A.cuLaunchKernel(ff, (unsigned)grid_for(mesh->n_faces, 128), 1, 1, 128, 1, 1, 0, (cudaStream_t)stream,
+                           args, nullptr) != 0)
+        return fail(PDG_ERR_CUDA, "cuLaunchKernel(pdg_jit_face_prepass) failed");
+      note_launch();
+    }
     return PDG_OK;
   }
   PDG_CATCH

@@ -11,193 +11,21 @@
 // sigma needs the a_bar of BOTH sides before any face term can be formed, so
 // it runs as a separate, cheap launch ahead of the element kernel.
 #include "pdg_internal.cuh"
+#include "prepass_body.cuh"
 
 namespace pdg {
 
 template <int DIM>
-__device__ __forceinline__ double nAn(const pdg_coeffs& C, const double* n, const double* x) {
-  if (C.diffusion_kind == PDG_DIFF_ISO) {
-    const double a = eval_prog(C, C.diffusion[0], x);
-    double s = 0.0;
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) s += n[i] * a * n[i];
-    return s;
-  }
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < DIM; ++i) {
-    double r = 0.0;
-#pragma unroll
-    for (int j = 0; j < DIM; ++j) r += eval_prog(C, C.diffusion[i * DIM + j], x) * n[j];
-    s += n[i] * r;
-  }
-  return s;
-}
-
-__device__ __forceinline__ bool diffusion_is_constant(const pdg_coeffs& C, int dim) {
-  if (C.diffusion_kind == PDG_DIFF_ISO) return C.diffusion[0].is_const;
-  for (int k = 0; k < dim * dim; ++k)
-    if (!C.diffusion[k].is_const) return false;
-  return true;
-}
-
-// max over an element's volume quadrature points of a(x) (isotropic a(x) I):
-// one warp per element, lanes over points, warp max.
-template <int DIM>
 __global__ void elem_abar_iso(const pdg_mesh m, const pdg_basis B, const __grid_constant__ pdg_coeffs C,
                               const pdg_rules R, const pdg_params prm, double* abar, uint32_t* flags) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < m.n_elements; e += nwarps) {
-    const int order = 2 * B.degree[e] + prm.quad_increment;
-    const int r0 = R.vol_offset[order], nq = R.vol_count[order];
-    const int64_t s0 = m.elem_ptr[e];
-    const int64_t Q = (m.elem_ptr[e + 1] - s0) * nq;
-    double best = -INFINITY;
-    for (int64_t g = lane; g < Q; g += 32) {
-      const int s = m.elem_simplices[s0 + g / nq];
-      const int k = (int)(g % nq);
-      double v0[3], E[3][3];
-      simplex_frame<DIM>(m, s, v0, E, flags);
-      double x[3] = {0, 0, 0};
-      const double* xi = R.points + (int64_t)(r0 + k) * 3;
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        double acc = v0[i];
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) acc += xi[j] * E[j][i];
-        x[i] = acc;
-      }
-      best = fmax(best, eval_prog(C, C.diffusion[0], x));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if (lane == 0) abar[e] = best;
-  }
-}
-
-template <int DIM>
-__device__ double side_abar(const pdg_mesh& m, const pdg_basis& B, const pdg_coeffs& C,
-                            const pdg_rules& R, const pdg_params& prm, const double* abar_iso,
-                            int32_t el, const double* n, uint32_t* flags) {
-  if (C.diffusion_kind == PDG_DIFF_NONE) return 0.0;
-  double x0[3] = {0, 0, 0};
-  if (diffusion_is_constant(C, DIM)) return nAn<DIM>(C, n, x0);
-  if (C.diffusion_kind == PDG_DIFF_ISO) {
-    double nn = 0.0;
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) nn += n[i] * n[i];
-    return abar_iso[el] * nn;
-  }
-  // general variable tensor: loop over the element's volume points
-  const int order = 2 * B.degree[el] + prm.quad_increment;
-  const int r0 = R.vol_offset[order], nq = R.vol_count[order];
-  double best = -INFINITY;
-  for (int64_t si = m.elem_ptr[el]; si < m.elem_ptr[el + 1]; ++si) {
-    double v0[3], E[3][3];
-    simplex_frame<DIM>(m, m.elem_simplices[si], v0, E, flags);
-    for (int k = 0; k < nq; ++k) {
-      const double* xi = R.points + (int64_t)(r0 + k) * 3;
-      double x[3] = {0, 0, 0};
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        double acc = v0[i];
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) acc += xi[j] * E[j][i];
-        x[i] = acc;
-      }
-      best = fmax(best, nAn<DIM>(C, n, x));
-    }
-  }
-  return best;
+  elem_abar_body<DIM>(m, B, InterpCoef<DIM>(C), R, prm, abar, flags);
 }
 
 template <int DIM>
 __global__ void face_prepass(const pdg_mesh m, const pdg_basis B, const __grid_constant__ pdg_coeffs C,
                              const pdg_rules R, const pdg_params prm, const double* abar_iso,
                              double* sigma, int8_t* flow, uint32_t* flags) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < m.n_faces; f += stride) {
-    const int32_t o = m.face_owner[f], nb = m.face_neighbor[f];
-    const int tag = m.face_tag[f];
-    const bool interior = nb >= 0;
-    double n[3] = {0, 0, 0};
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) n[i] = m.face_normal[f * DIM + i];
-    sigma[f] = 0.0;
-    flow[f] = interior ? -1 : 0;
-    if (!interior && tag == PDG_TAG_INTERIOR) {
-      raise_flag(flags, PDG_FLAG_UNCLASSIFIED);
-      continue;
-    }
-    if (!interior && tag != PDG_TAG_DIRICHLET) continue;  // inflow/neumann/outflow need neither
-
-    // -- flow side: order-2 sample points of every sub-facet
-    if (C.has_advection) {
-      const int r0 = R.face_offset[2], nq = R.face_count[2];
-      double sum = 0.0, mn = INFINITY, mx = -INFINITY, amax = 0.0;
-      int cnt = 0;
-      for (int64_t row = m.face_ptr[f]; row < m.face_ptr[f + 1]; ++row) {
-        double v0[3], E[3][3];
-        facet_frame<DIM>(m, row, v0, E, flags);
-        for (int k = 0; k < nq; ++k) {
-          const double* xi = R.points + (int64_t)(r0 + k) * 3;
-          double x[3] = {0, 0, 0};
-#pragma unroll
-          for (int i = 0; i < DIM; ++i) {
-            double acc = v0[i];
-#pragma unroll
-            for (int j = 0; j < DIM - 1; ++j) acc += xi[j] * E[j][i];
-            x[i] = acc;
-          }
-          double bn = 0.0;
-#pragma unroll
-          for (int i = 0; i < DIM; ++i) bn += eval_prog(C, C.advection[i], x) * n[i];
-          sum += bn;
-          mn = fmin(mn, bn);
-          mx = fmax(mx, bn);
-          amax = fmax(amax, fabs(bn));
-          ++cnt;
-        }
-      }
-      const double tol = 1e-10 * fmax(1.0, amax);
-      if (mn < -tol && mx > tol) raise_flag(flags, PDG_FLAG_STRADDLE);
-      const double mean = sum / cnt;
-      if (interior) flow[f] = mean < 0.0 ? 0 : (mean > 0.0 ? 1 : -1);
-      else flow[f] = mean < 0.0 ? 1 : 0;
-    }
-
-    // -- penalty
-    double best = 0.0;
-    for (int side = 0; side < (interior ? 2 : 1); ++side) {
-      const int32_t el = side == 0 ? o : nb;
-      double mxv = -1.0;
-      bool any = false;
-      for (int64_t row = m.face_ptr[f]; row < m.face_ptr[f + 1]; ++row) {
-        const int32_t s = side == 0 ? m.facet_owner_simplex[row] : m.facet_neighbor_simplex[row];
-        if (s < 0) continue;
-        const double v = m.simplex_volumes[s];
-        mxv = any ? fmax(mxv, v) : v;
-        any = true;
-      }
-      if (!any || !(mxv > 0.0)) {
-        raise_flag(flags, PDG_FLAG_NO_ADJACENT_SIMPLEX);
-        continue;
-      }
-      const int p = B.degree[el];
-      const double vol = m.elem_volumes[el];
-      double cap = INFINITY;
-      if (prm.coverable && prm.coverable[el]) {
-        double c = 1.0;
-        for (int k = 0; k < 2 * (DIM - 1); ++k) c *= (double)p;
-        cap = c;
-      }
-      const double ab = side_abar<DIM>(m, B, C, R, prm, abar_iso, el, n, flags);
-      const double ratio = fmin(vol / mxv, cap);
-      best = fmax(best, ratio * ab * (double)(p * p) * m.face_measure[f] / vol);
-    }
-    sigma[f] = prm.penalty_constant * best;
-  }
+  face_prepass_body<DIM>(m, B, InterpCoef<DIM>(C), R, prm, abar_iso, sigma, flow, flags);
 }
 
 // Interface records (pdg_iface_rec) of the owned rows: one warp per row

@@ -72,6 +72,32 @@ __device__ __forceinline__ double eval_prog(const pdg_coeffs& C, const pdg_prog&
   return eval_prog_slow(C, p, x[0], x[1], x[2]);
 }
 
+// Ahead-of-time coefficient policy: interprets the bytecode in pdg_coeffs.
+template <int DIM>
+struct InterpCoef {
+  const pdg_coeffs& C;
+  __device__ InterpCoef(const pdg_coeffs& c) : C(c) {}
+  __device__ int diff_kind() const { return C.diffusion_kind; }
+  __device__ bool a_const() const {
+    if (C.diffusion_kind == PDG_DIFF_ISO) return C.diffusion[0].is_const;
+    for (int k = 0; k < DIM * DIM; ++k)
+      if (!C.diffusion[k].is_const) return false;
+    return true;
+  }
+  __device__ bool has_adv() const { return C.has_advection; }
+  __device__ bool has_reac() const { return C.has_reaction; }
+  __device__ bool has_src() const { return C.has_source; }
+  __device__ bool has_dir() const { return C.has_dirichlet; }
+  __device__ bool has_neu() const { return C.has_neumann; }
+  __device__ double a_iso(const double* x) const { return eval_prog(C, C.diffusion[0], x); }
+  __device__ double a_ij(int i, int j, const double* x) const { return eval_prog(C, C.diffusion[i * DIM + j], x); }
+  __device__ double b_i(int i, const double* x) const { return eval_prog(C, C.advection[i], x); }
+  __device__ double c(const double* x) const { return eval_prog(C, C.reaction, x); }
+  __device__ double f(const double* x) const { return eval_prog(C, C.source, x); }
+  __device__ double gD(const double* x) const { return eval_prog(C, C.dirichlet, x); }
+  __device__ double gN(const double* x) const { return eval_prog(C, C.neumann, x); }
+};
+
 // ---------------------------------------------------------------------------
 // compile-time basis tables (graded-lex multi-indices, basis.py:86-104)
 // ---------------------------------------------------------------------------

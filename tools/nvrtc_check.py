@@ -20,9 +20,17 @@ def main(cfg="cfg5", degree=None, sym=True, minblocks=3, ws="0"):
     mr = os.environ.get("PDG_JIT_MAXNREG")
     bounds = f"__maxnreg__({mr})" if mr else f"__launch_bounds__({threads}, {minblocks})"
     tail = ", pdg_jit::JitCoef, 32" if body == "assemble_body" else ""
-    src = (f'#include "{body}.cuh"\nnamespace pdg_jit {{\nusing namespace pdg;\n' + pol + '\n}\n'
+    src = (f'#include "{body}.cuh"\n#include "prepass_body.cuh"\nnamespace pdg_jit {{\nusing namespace pdg;\n'
+           + pol + '\n}\n'
            f'extern "C" __global__ void {bounds} pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {{\n'
-           f'  pdg::{body}<{w.dim}, {p}, {"true" if sym else "false"}{tail}>(a, pdg_jit::JitCoef());\n}}\n')
+           f'  pdg::{body}<{w.dim}, {p}, {"true" if sym else "false"}{tail}>(a, pdg_jit::JitCoef());\n}}\n'
+           'extern "C" __global__ void __launch_bounds__(128) pdg_jit_face_prepass(const pdg_mesh m, '
+           'const pdg_basis B, const pdg_rules R, const pdg_params prm, const double* abar, double* sigma, '
+           'int8_t* flow, uint32_t* flags) {\n'
+           f'  pdg::face_prepass_body<{w.dim}>(m, B, pdg_jit::JitCoef(), R, prm, abar, sigma, flow, flags);\n}}\n'
+           'extern "C" __global__ void __launch_bounds__(256) pdg_jit_abar(const pdg_mesh m, const pdg_basis B, '
+           'const pdg_rules R, const pdg_params prm, double* abar, uint32_t* flags) {\n'
+           f'  pdg::elem_abar_body<{w.dim}>(m, B, pdg_jit::JitCoef(), R, prm, abar, flags);\n}}\n')
     lib = C.CDLL("libnvrtc.so.12")
     prog = C.c_void_p()
     assert lib.nvrtcCreateProgram(C.byref(prog), src.encode(), b"pdg_jit.cu", 0, None, None) == 0
