@@ -40,22 +40,27 @@ template <int DIM>
 __global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, const pdg_basis B, const pdg_rules R,
                                                             int inc, int has_adv, const pdg_pattern P,
                                                             const double* sigma, const int8_t* flow) {
+  // 8-lane groups, one row element each (4 per warp): a Voronoi cell has ~7
+  // neighbours, so a whole warp per element would leave 3/4 of the lanes idle
+  constexpr int GL = 8;
   __shared__ int4 stage[4][32 * 5];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  int4* st = stage[wib];
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < P.n_row_elements; k += nwarps) {
+  const int grp = lane / GL, gl = lane % GL;
+  const unsigned gmask = 0xffu << (grp * GL);
+  int4* st = stage[wib] + grp * GL * 5;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / GL;
+  for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / GL; k < P.n_row_elements; k += ngroups) {
     const int32_t e = P.row_elements ? P.row_elements[k] : (int32_t)k;
     const int pe = B.degree[e];
     const int64_t q0 = P.nbr_ptr[e], q1 = P.nbr_ptr[e + 1];
     int carry = 0;
-    for (int64_t c0 = q0; c0 < q1; c0 += 32) {
-      const int nv = (int)(q1 - c0 < 32 ? q1 - c0 : 32);
-      const int64_t q = c0 + lane;
+    for (int64_t c0 = q0; c0 < q1; c0 += GL) {
+      const int nv = (int)(q1 - c0 < GL ? q1 - c0 : GL);
+      const int64_t q = c0 + gl;
       int j = 0, nj = 0, pj = 0, fa = 0, fb = 0, row0 = 0, info = 0, nrows = 0;
       double sig = 0.0, nrm[3] = {0.0, 0.0, 0.0};
       long long dof = 0;
-      if (lane < nv) {
+      if (gl < nv) {
         j = P.nbr_elem[q];
         dof = B.dof_offset[j];
         nj = (int)(B.dof_offset[j + 1] - dof);
@@ -76,17 +81,17 @@ __global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, co
           for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)fa * DIM + i];
         }
       }
-      // exclusive scan of nj over the chunk
+      // exclusive scan of nj over the group's chunk
       int incl = nj;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
+      for (int o = 1; o < GL; o <<= 1) {
+        const int v = __shfl_up_sync(gmask, incl, o, GL);
+        if (gl >= o) incl += v;
       }
       const int col = carry + incl - nj;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-      if (lane < nv) {
-        int4* r = st + lane * 5;
+      carry += __shfl_sync(gmask, incl, GL - 1, GL);
+      if (gl < nv) {
+        int4* r = st + gl * 5;
         r[0] = make_int4(j, nj, col, pj);
         r[1] = make_int4(fa, fb, row0, info);
         double2* rd = reinterpret_cast<double2*>(r + 2);
@@ -95,10 +100,10 @@ __global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, co
         // first-face row count: read by the 3D element kernel only
         reinterpret_cast<longlong2*>(r + 4)[0] = make_longlong2(dof, DIM == 3 ? (long long)(unsigned)nrows : 0ll);
       }
-      __syncwarp();
+      __syncwarp(gmask);
       int4* dst = reinterpret_cast<int4*>(P.nbr_rec + c0);
-      for (int c = lane; c < nv * 5; c += 32) dst[c] = st[c];
-      __syncwarp();
+      for (int c = gl; c < nv * 5; c += GL) dst[c] = st[c];
+      __syncwarp(gmask);
     }
   }
 }
@@ -116,7 +121,7 @@ extern "C" int pdg_iface_records(const pdg_mesh* mesh, const pdg_basis* basis, c
       return fail(PDG_ERR_INVALID, "null argument");
     if (pattern->n_row_elements <= 0) return PDG_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const int grid = grid_for_warps(pattern->n_row_elements, 128);
+    const int grid = grid_for_warps((pattern->n_row_elements + 3) / 4, 128);
     if (mesh->dim == 2)
       iface_records_kernel<2><<<grid, 128, 0, st>>>(*mesh, *basis, *rules, params->quad_increment,
                                                     coeffs->has_advection, *pattern, sigma, face_flow);
@@ -178,45 +183,76 @@ extern "C" int pdg_face_prepass(const pdg_mesh* mesh, const pdg_basis* basis, co
 // ---------------------------------------------------------------------------
 namespace pdg {
 
+// Records are assembled per warp in shared memory and written as contiguous
+// 16-byte chunks (32 records of W doubles per warp), so every DRAM sector is
+// written whole by one instruction stream.
 template <int DIM>
-__global__ void frames_kernel(const pdg_mesh m, const pdg_basis B, const pdg_frames F, uint32_t* flags) {
+__global__ void __launch_bounds__(256) frames_kernel(const pdg_mesh m, const pdg_basis B, const pdg_frames F,
+                                                     uint32_t* flags) {
   constexpr int W = DIM == 2 ? 8 : 16;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (int64_t i = tid; i < m.n_simplices; i += stride) {
-    double v0[3], E[3][3];
-    const double det = simplex_frame<DIM>(m, m.elem_simplices[i], v0, E, flags);
-    double* o = F.simplex + i * W;
+  __shared__ double stage[8][32 * W];
+  const int lane = threadIdx.x & 31;
+  double* sw = stage[threadIdx.x >> 5];
+  double* o = sw + lane * W;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  auto flush = [&](double* dst, int64_t base, int64_t n) {
+    __syncwarp();
+    const int nv = (int)(n - base < 32 ? n - base : 32);
+    double2* d = reinterpret_cast<double2*>(dst + base * W);
+    const double2* src = reinterpret_cast<const double2*>(sw);
+    for (int c = lane; c < nv * W / 2; c += 32) d[c] = src[c];
+    __syncwarp();
+  };
+  for (int64_t base = w0 * 32; base < m.n_simplices; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    if (i < m.n_simplices) {
+      double v0[3], E[3][3];
+      const double det = simplex_frame<DIM>(m, m.elem_simplices[i], v0, E, flags);
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) o[d] = v0[d];
+      for (int d = 0; d < DIM; ++d) o[d] = v0[d];
 #pragma unroll
-    for (int k = 0; k < DIM; ++k)
+      for (int k = 0; k < DIM; ++k)
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
-    o[DIM + DIM * DIM] = det;
-    o[DIM + DIM * DIM + 1] = sqrt(det);  // sqrt-weighted volume tables (assemble_body.cuh)
-  }
-  for (int64_t r = tid; r < m.n_facets; r += stride) {
-    double v0[3], E[3][3];
-    const double jac = facet_frame<DIM>(m, r, v0, E, flags);
-    double* o = F.facet + r * W;
+        for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
+      o[DIM + DIM * DIM] = det;
+      o[DIM + DIM * DIM + 1] = sqrt(det);  // sqrt-weighted volume tables (assemble_body.cuh)
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) o[d] = v0[d];
-#pragma unroll
-    for (int k = 0; k < DIM - 1; ++k)
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
-    o[DIM + (DIM - 1) * DIM] = jac;
-  }
-  for (int64_t e = tid; e < m.n_elements; e += stride) {
-    const BoxConst<DIM> b = box_const<DIM>(B.box + e * 2 * DIM);
-    double* o = F.element + e * W;
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      o[d] = b.c[d];
-      o[DIM + d] = b.ih[d];
-      o[2 * DIM + d] = b.rs[d];
+      for (int c = DIM + DIM * DIM + 2; c < W; ++c) o[c] = 0.0;
     }
+    flush(F.simplex, base, m.n_simplices);
+  }
+  for (int64_t base = w0 * 32; base < m.n_facets; base += nwarps * 32) {
+    const int64_t r = base + lane;
+    if (r < m.n_facets) {
+      double v0[3], E[3][3];
+      const double jac = facet_frame<DIM>(m, r, v0, E, flags);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) o[d] = v0[d];
+#pragma unroll
+      for (int k = 0; k < DIM - 1; ++k)
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) o[DIM + k * DIM + d] = E[k][d];
+      o[DIM + (DIM - 1) * DIM] = jac;
+#pragma unroll
+      for (int c = DIM + (DIM - 1) * DIM + 1; c < W; ++c) o[c] = 0.0;
+    }
+    flush(F.facet, base, m.n_facets);
+  }
+  for (int64_t base = w0 * 32; base < m.n_elements; base += nwarps * 32) {
+    const int64_t e = base + lane;
+    if (e < m.n_elements) {
+      const BoxConst<DIM> b = box_const<DIM>(B.box + e * 2 * DIM);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        o[d] = b.c[d];
+        o[DIM + d] = b.ih[d];
+        o[2 * DIM + d] = b.rs[d];
+      }
+#pragma unroll
+      for (int c = 3 * DIM; c < W; ++c) o[c] = 0.0;
+    }
+    flush(F.element, base, m.n_elements);
   }
 }
 
@@ -230,8 +266,9 @@ extern "C" int pdg_frames_build(const pdg_mesh* mesh, const pdg_basis* basis, co
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = std::max(mesh->n_simplices, std::max(mesh->n_facets, mesh->n_elements));
     if (n == 0) return PDG_OK;
-    if (mesh->dim == 2) frames_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(*mesh, *basis, *frames, err_flags);
-    else if (mesh->dim == 3) frames_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(*mesh, *basis, *frames, err_flags);
+    const int grid = grid_for_warps((n + 31) / 32, 256);
+    if (mesh->dim == 2) frames_kernel<2><<<grid, 256, 0, st>>>(*mesh, *basis, *frames, err_flags);
+    else if (mesh->dim == 3) frames_kernel<3><<<grid, 256, 0, st>>>(*mesh, *basis, *frames, err_flags);
     else return fail(PDG_ERR_UNSUPPORTED, "dim must be 2 or 3");
     note_launch();
     PDG_CUDA(cudaGetLastError());
