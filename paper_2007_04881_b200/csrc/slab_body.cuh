@@ -337,14 +337,24 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
     slab_zero<TR, TC>(cd);
 
     // RHS contribution of a round: rhs_s[f] += sum_slot V[f] r1 + F[f] r2 (one owner per f)
+    // (every weight carries the slot's valid factor, so all 32 slots are summed:
+    // a fixed trip count the compiler pipelines)
     auto rhs_round = [&](int rowV, int rowF, int nvalid, bool useF) {
-      for (int f = threadIdx.x; f < NB; f += NW * 32) {
-        double s = 0.0;
-        for (int l = 0; l < nvalid; ++l) {
-          s += TAB(rowV, f, l) * r1_[l];
-          if (useF) s += TAB(rowF, f, l) * r2_[l];
+      (void)nvalid;
+      {
+        for (int f = threadIdx.x; f < NB; f += NW * 32) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+          for (int l = 0; l < SLAB_KS; l += 2) {
+            s0 += TAB(rowV, f, l) * r1_[l];
+            s1 += TAB(rowV, f, l + 1) * r1_[l + 1];
+            if (useF) {
+              s0 += TAB(rowF, f, l) * r2_[l];
+              s1 += TAB(rowF, f, l + 1) * r2_[l + 1];
+            }
+          }
+          rhs_s[f] += s0 + s1;
         }
-        rhs_s[f] += s;
       }
     };
 
