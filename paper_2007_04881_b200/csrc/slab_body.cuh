@@ -521,9 +521,8 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
     };
     // C_aa += L1 V_a^T + L2 F_a^T, C_ab += L1 (-V_b)^T + L2 F_b^T with
     // L1 = alpha V_a + beta F_a, L2 = beta V_a (assemble_body.cuh header)
-    auto face_contract = [&](int nvalid, bool two, bool useF, double (&co)[TR][TC][2]) {
-      const int nk = (nvalid + 3) >> 2;
-      for (int kk = wk; kk < nk; kk += WK) {
+    auto face_contract_k = [&](int k0, int nk, bool two, bool useF, double (&co)[TR][TC][2]) {
+      for (int kk = k0 + wk; kk < nk; kk += WK) {
         const int q = kk * 4 + t;
         const double al = s0_[q], be = s1_[q];
         double l1[TR], l2[TR];
@@ -559,11 +558,78 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         }
       }
     };
+    auto face_contract = [&](int nvalid, bool two, bool useF, double (&co)[TR][TC][2]) {
+      face_contract_k(0, (nvalid + 3) >> 2, two, useF, co);
+    };
 
     // ------------------------------------------------------ lateral interfaces
-    for (int qn = 0; qn < min(nnb, SLAB_NBR_MAX); ++qn) {
+    const int nnw = min(nnb, SLAB_NBR_MAX);
+    for (int qn = 0; qn < nnw; ++qn) {
       const int32_t j = nb_j[qn];
       if (j == e) continue;
+      // Two single-face, single-sub-facet interfaces with <= 16 lateral points
+      // each (every 2D Voronoi interface at p <= 2) share one 32-slot round:
+      // slots 0-15 the first, 16-31 the second (diagonal block over both,
+      // off-diagonal blocks over their own k-steps).
+      {
+        int qb = qn + 1;
+        if (qb < nnw && nb_j[qb] == e) ++qb;
+        auto small = [&](int q) {
+          const int o = 2 * max(pe, nb_pj[q]) + a.prm.quad_increment;
+          return (nb_info[q] & 4) && R.face_count[o] <= 4;
+        };
+        if (qb < nnw && small(qn) && small(qb)) {
+          {
+            const int seg = lane >> 4, ls = lane & 15;
+            const int q = seg ? qb : qn;
+            const int o = 2 * max(pe, nb_pj[q]) + a.prm.quad_increment;
+            const int r0e = R.face_offset[o], nqe = R.face_count[o];
+            const int nqf = nqe * nqe;
+            const double valid = ls < nqf ? 1.0 : 0.0;
+            const int gq = min(ls, nqf - 1);
+            const int ie = gq / nqe, it = gq - ie * nqe;
+            const int side = nb_info[q] & 1;
+            const double sgn = side ? -1.0 : 1.0;
+            const bool down = CF::has_adv() && (nb_info[q] & 2) != 0;
+            const double nrm[3] = {nb_n0[q], nb_n1[q], 0.0};
+            double x[3];
+            const double jac =
+                frame_point<2, 1>(a.fframe + (int64_t)nb_row0[q] * 8, R.points + (r0e + ie) * 3, x);
+            x[2] = t0 + tau * R.points[(r0e + it) * 3];
+            const double w = (R.weights[r0e + ie] * jac) * (tau * R.weights[r0e + it]) * valid;
+            SlabTab<P, PQ> ta, tn;
+            ta.load(bx, x);
+            tn.load(slab_box(a.erec, nb_j[q], tbox), x);
+            face_tab(ta, tn, nrm, x, true, grad_terms);
+            if (warp == 0) {
+              double wbn = 0.0;
+              if (down) {
+                double bn = 0.0;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                  if (CF::b_nz(i)) bn += cf.b_i(i, x) * nrm[i];
+                wbn = w * bn;
+              }
+              s0_[lane] = w * nb_sig[q] - sgn * wbn;
+              s1_[lane] = grad_terms ? -0.5 * sgn * w : 0.0;
+            }
+          }
+          __syncthreads();
+          // both halves contracted before any split-K reduction (it reuses the table)
+          double co[TR][TC][2], co2[TR][TC][2];
+          slab_zero<TR, TC>(co);
+          slab_zero<TR, TC>(co2);
+          face_contract_k(0, 4, true, grad_terms, co);
+          face_contract_k(4, 8, true, grad_terms, co2);
+          slab_reduce<TR, TC, WK, WR * WC>(co, red, wk, wr + WR * wc, lane);
+          if (wk == 0) slab_store<TR, TC>(a.values, voff, Lrow, nb_col[qn], ne, nb_n[qn], co, wr, wc, g, t);
+          slab_reduce<TR, TC, WK, WR * WC>(co2, red, wk, wr + WR * wc, lane);
+          if (wk == 0) slab_store<TR, TC>(a.values, voff, Lrow, nb_col[qb], ne, nb_n[qb], co2, wr, wc, g, t);
+          __syncthreads();
+          qn = qb;
+          continue;
+        }
+      }
       const int pj = nb_pj[qn];
       const BoxConst<3> bo = slab_box(a.erec, j, tbox);
       const int order = 2 * max(pe, pj) + a.prm.quad_increment;
