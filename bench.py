@@ -379,17 +379,19 @@ def run_ours(args, w, rank, world, local_rank):
         e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
         del io
 
+    cdev = dev if world == 1 or dist.get_backend() == "nccl" else torch.device("cpu")
+
     def allmax(x):
         if world == 1 or x is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def allsum(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -464,8 +466,15 @@ def main():
         import torch
         import torch.distributed as dist
 
+        # PDG_DIST_BACKEND=gloo + fewer GPUs than ranks: ranks share devices
+        # (exercises the partitioned path on a 1-GPU box; NCCL needs one GPU per rank)
+        backend = os.environ.get("PDG_DIST_BACKEND", "nccl")
+        local_rank = local_rank % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     run_ours(args, w, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
