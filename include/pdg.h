@@ -227,6 +227,7 @@ typedef struct pdg_slab {
   const double* prev_box;         /* [n_elements][2][3] previous slab prism boxes */
   int32_t family;                 /* basis family of the slab: 0 = P, 1 = PQ (basis.py:21-26) */
   int32_t table_rows;             /* shared table rows of the coefficient set (model.slab_policy) */
+  pdg_rules time_rules;           /* interval rules (in the face tables) of the time axis */
 } pdg_slab;
 
 /* Approach-1 work items (see pdg_a1_emit). */
@@ -330,14 +331,14 @@ int pdg_jit_prepare(const pdg_coeffs* coeffs, const char* policy_source, int32_t
  * The index phase is shared with the spatial path (pdg_adjacency /
  * pdg_pattern_offsets with the slab basis), as are the spatial affine frames
  * (pdg_frames_build).  policy_source: model.slab_policy (coefficients in
- * (x, y, t) + initial data).  Spatial dimension 2 (prisms in 3D), degree
+ * (x, y[, z], t) + initial data).  Spatial dimension 2 or 3, degree
  * <= PDG_SLAB_MAX_DEGREE (family P) / PDG_SLAB_MAX_DEGREE_PQ, uniform degree
  * for family PQ. */
 #define PDG_SLAB_MAX_DEGREE 5
 #define PDG_SLAB_MAX_DEGREE_PQ 4
 
 /* Compile (or fetch) the slab kernels of one coefficient set / degree / family. */
-int pdg_slab_prepare(const char* policy_source, int32_t max_degree, int32_t family);
+int pdg_slab_prepare(const char* policy_source, int32_t spatial_dim, int32_t max_degree, int32_t family);
 
 /* Lateral face pre-pass: penalty sigma with the slab's side data
  * (spacetime.py:301-351) and the flow side (spacetime.py:287-309) of every

@@ -92,7 +92,8 @@ class Frames(C.Structure):
 
 class Slab(C.Structure):
     _fields_ = [("t0", _f64), ("t1", _f64), ("lateral_tag", _p), ("prev_values", _p),
-                ("prev_dof_offset", _p), ("prev_box", _p), ("family", _i32), ("table_rows", _i32)]
+                ("prev_dof_offset", _p), ("prev_box", _p), ("family", _i32), ("table_rows", _i32),
+                ("time_rules", Rules)]
 
 
 class A1Items(C.Structure):
@@ -155,7 +156,7 @@ def load():
     lib.pdg_face_prepass_jit.argtypes = [P(Mesh), P(Basis), P(Coeffs), C.c_char_p, P(Rules), P(Params),
                                          _p, _p, _p, _p, _p]
     lib.pdg_jit_prepare.argtypes = [P(Coeffs), C.c_char_p, _i32, _i32]
-    lib.pdg_slab_prepare.argtypes = [C.c_char_p, _i32, _i32]
+    lib.pdg_slab_prepare.argtypes = [C.c_char_p, _i32, _i32, _i32]
     lib.pdg_slab_prepass.argtypes = [P(Mesh), P(Basis), C.c_char_p, P(Rules), P(Params), P(Slab),
                                      P(Frames), _p, _p, _p, _p]
     lib.pdg_slab_assemble.argtypes = [P(Mesh), P(Basis), C.c_char_p, P(Rules), P(Params), P(Slab),

@@ -411,49 +411,51 @@ extern "C" int pdg_face_prepass_jit(const pdg_mesh* mesh, const pdg_basis* basis
 // ---------------------------------------------------------------------------
 namespace pdg {
 
-static int slab_nb(int P, int fam) { return fam ? (P + 1) * binom(P + 2, 2) : binom(P + 3, 3); }
+static int slab_nb(int S, int P, int fam) { return fam ? (P + 1) * binom(P + S, S) : binom(P + S + 1, S + 1); }
 
 // PDG_SLAB_WARPS: warps per CTA of the slab kernel (1, 2 or 4); default by the
 // row block's tile count (measured, 200k-prism slabs, family P, r01:
 // p=1 1/2/4 warps 4.47/5.74/10.5 ms, p=2 11.3/15.7/25.5, p=3 36.7/39.9/55.2,
 // p=4 -/148.7/170.7): one warp up to 3x3 tiles, two up to 6x6, else four
-static int slab_warps(int P, int fam) {
+static int slab_warps(int S, int P, int fam) {
   if (const char* v = getenv("PDG_SLAB_WARPS")) {
     const int w = atoi(v);
     if (w == 1 || w == 2 || w == 4) return w;
   }
-  const int nt = (slab_nb(P, fam) + 7) / 8;
+  const int nt = (slab_nb(S, P, fam) + 7) / 8;
   return nt <= 3 ? 1 : (nt <= 6 ? 2 : 4);
 }
 
-static std::string slab_source(const std::string& policy, int P, int fam, int nw) {
+static std::string slab_source(const std::string& policy, int S, int P, int fam, int nw) {
   std::ostringstream os;
   os << "#include \"slab_body.cuh\"\n"
      << "namespace pdg_jit {\nusing namespace pdg;\n" << policy << "\n}\n"
      << "extern \"C\" __global__ void __launch_bounds__(" << 32 * nw << ", 1) "
      << "pdg_slab_kernel(const __grid_constant__ pdg::SlabArgs a) {\n"
-     << "  pdg::slab_body<" << P << ", " << (fam ? "true" : "false") << ", " << nw
+     << "  pdg::slab_body<" << S << ", " << P << ", " << (fam ? "true" : "false") << ", " << nw
      << ", pdg_jit::JitCoef>(a, pdg_jit::JitCoef());\n}\n"
      << "extern \"C\" __global__ void __launch_bounds__(128) "
      << "pdg_slab_prepass(const __grid_constant__ pdg::SlabArgs a, double* sigma, int8_t* flow) {\n"
-     << "  pdg::slab_prepass_body(a, pdg_jit::JitCoef(), sigma, flow);\n}\n";
+     << "  pdg::slab_prepass_body<" << S << ">(a, pdg_jit::JitCoef(), sigma, flow);\n}\n";
   return os.str();
 }
 
-static std::string slab_module(const char* policy, int P, int fam, CUmod& mod) {
+static std::string slab_module(const char* policy, int S, int P, int fam, CUmod& mod) {
   const int pmax = fam ? PDG_SLAB_MAX_DEGREE_PQ : PDG_SLAB_MAX_DEGREE;
   if (P < 0 || P > pmax)
     return "slab degree " + std::to_string(P) + " outside the supported range 0.." + std::to_string(pmax) +
            (fam ? " (family PQ)" : " (family P)");
-  return get_module(slab_source(policy, P, fam, slab_warps(P, fam)), mod);
+  if (S != 2 && S != 3) return "slab spatial dimension must be 2 or 3";
+  return get_module(slab_source(policy, S, P, fam, slab_warps(S, P, fam)), mod);
 }
 
 static int slab_check(const pdg_mesh* mesh, const pdg_basis* basis, const char* policy, const pdg_rules* rules,
                       const pdg_params* params, const pdg_slab* slab) {
   if (!mesh || !basis || !policy || !rules || !params || !slab) return fail(PDG_ERR_INVALID, "null argument");
-  if (mesh->dim != 2) return fail(PDG_ERR_UNSUPPORTED, "slabs need a 2D spatial mesh (prisms in 3D)");
+  if (mesh->dim != 2 && mesh->dim != 3) return fail(PDG_ERR_UNSUPPORTED, "slabs need a 2D or 3D spatial mesh");
+  if (!slab->time_rules.points || !slab->time_rules.face_offset) return fail(PDG_ERR_INVALID, "time rules missing");
   if (!slab->lateral_tag) return fail(PDG_ERR_INVALID, "lateral tags missing");
-  if (slab->table_rows < 4 || slab->table_rows > 8) return fail(PDG_ERR_INVALID, "table_rows must be 4..8");
+  if (slab->table_rows < 4 || slab->table_rows > 10) return fail(PDG_ERR_INVALID, "table_rows must be 4..10");
   if (!(slab->t1 > slab->t0)) return fail(PDG_ERR_INVALID, "slab interval must have positive length");
   if (slab->prev_values && (!slab->prev_dof_offset || !slab->prev_box))
     return fail(PDG_ERR_INVALID, "previous slab data incomplete");
@@ -470,6 +472,7 @@ static SlabArgs slab_args(const pdg_mesh* mesh, const pdg_basis* basis, const pd
   a.R = *rules;
   a.prm = *params;
   a.sl = *slab;
+  a.T = slab->time_rules;
   a.sframe = frames->simplex;
   a.fframe = frames->facet;
   a.erec = frames->element;
@@ -481,11 +484,12 @@ static SlabArgs slab_args(const pdg_mesh* mesh, const pdg_basis* basis, const pd
 
 }  // namespace pdg
 
-extern "C" int pdg_slab_prepare(const char* policy_source, int32_t max_degree, int32_t family) {
+extern "C" int pdg_slab_prepare(const char* policy_source, int32_t spatial_dim, int32_t max_degree,
+                                int32_t family) {
   PDG_TRY {
     if (!policy_source) return fail(PDG_ERR_INVALID, "null argument");
     CUmod mod = nullptr;
-    const std::string err = slab_module(policy_source, max_degree, family, mod);
+    const std::string err = slab_module(policy_source, spatial_dim, max_degree, family, mod);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
     return PDG_OK;
   }
@@ -503,7 +507,7 @@ extern "C" int pdg_slab_prepass(const pdg_mesh* mesh, const pdg_basis* basis, co
       return fail(PDG_ERR_INVALID, "null argument");
     if (mesh->n_faces == 0) return PDG_OK;
     CUmod mod = nullptr;
-    std::string err = slab_module(policy_source, basis->max_degree, slab->family, mod);
+    std::string err = slab_module(policy_source, mesh->dim, basis->max_degree, slab->family, mod);
     CUfunc fn = nullptr;
     if (err.empty()) err = get_function(mod, "pdg_slab_prepass", fn);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
@@ -534,9 +538,9 @@ extern "C" int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, c
       return fail(PDG_ERR_INVALID, "pattern not built (pdg_adjacency / pdg_pattern_offsets)");
     if (!pattern->nbr_rec) return fail(PDG_ERR_INVALID, "interface records missing (pdg_iface_records)");
     if (pattern->n_row_elements <= 0) return PDG_OK;
-    const int P = basis->max_degree, fam = slab->family, nw = slab_warps(P, fam);
+    const int S = mesh->dim, P = basis->max_degree, fam = slab->family, nw = slab_warps(S, P, fam);
     CUmod mod = nullptr;
-    std::string err = slab_module(policy_source, P, fam, mod);
+    std::string err = slab_module(policy_source, S, P, fam, mod);
     CUfunc fn = nullptr;
     if (err.empty()) err = get_function(mod, "pdg_slab_kernel", fn);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
@@ -544,7 +548,7 @@ extern "C" int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, c
     a.pat = *pattern;
     a.values = values;
     a.rhs = rhs;
-    const int nb = slab_nb(P, fam), nt = (nb + 7) / 8;
+    const int nb = slab_nb(S, P, fam), nt = (nb + 7) / 8;
     const size_t smem = slab_smem_bytes(slab->table_rows, nt * 8, nt, nw);
     Api& A = api();
     if (A.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES_, (int)smem) != 0)

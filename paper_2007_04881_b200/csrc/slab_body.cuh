@@ -42,54 +42,67 @@ struct IC {
   static constexpr int value = N;
 };
 
-// multi-index table of the slab basis (basis.py:86-104): family P = graded
-// lex in (x, y, t); family PQ = spatial graded lex x time degree, time outer.
-template <int P, bool PQ>
+// multi-index table of the slab basis (basis.py:86-104) in D = S + 1
+// coordinates (time last): family P = graded lex in (x.., t); family PQ =
+// spatial graded lex x time degree, time outer.
+template <int S, int P, bool PQ>
 struct SlabMI {
-  static constexpr int NS = binom(P + 2, 2);
-  static constexpr int NB = PQ ? (P + 1) * NS : binom(P + 3, 3);
-  int a[NB][3];
+  static constexpr int D = S + 1;
+  static constexpr int NS = binom(P + S, S);
+  static constexpr int NB = PQ ? (P + 1) * NS : binom(P + D, D);
+  int a[NB][4];
+  // lex order of itertools.product(range(tot + 1), repeat=n) filtered by sum == tot
+  __host__ __device__ constexpr void glex(int n, int tot, int k, int& f) {
+    int total = 1;
+    for (int i = 0; i < n; ++i) total *= tot + 1;
+    for (int idx = 0; idx < total; ++idx) {
+      int dig[4] = {0, 0, 0, 0}, r = idx, sum = 0;
+      for (int i = n - 1; i >= 0; --i) {
+        dig[i] = r % (tot + 1);
+        r /= tot + 1;
+        sum += dig[i];
+      }
+      if (sum != tot) continue;
+      for (int i = 0; i < 4; ++i) a[f][i] = 0;
+      for (int i = 0; i < n; ++i) a[f][i] = dig[i];
+      if (k >= 0) a[f][S] = k;
+      ++f;
+    }
+  }
   __host__ __device__ constexpr SlabMI() : a{} {
     int f = 0;
     if (PQ) {
       for (int k = 0; k <= P; ++k)
-        for (int tot = 0; tot <= P; ++tot)
-          for (int i = 0; i <= tot; ++i) {
-            a[f][0] = i;
-            a[f][1] = tot - i;
-            a[f][2] = k;
-            ++f;
-          }
+        for (int tot = 0; tot <= P; ++tot) glex(S, tot, k, f);
     } else {
-      for (int tot = 0; tot <= P; ++tot)
-        for (int i = 0; i <= tot; ++i)
-          for (int j = 0; j <= tot - i; ++j) {
-            a[f][0] = i;
-            a[f][1] = j;
-            a[f][2] = tot - i - j;
-            ++f;
-          }
+      for (int tot = 0; tot <= P; ++tot) glex(D, tot, -1, f);
     }
   }
 };
 
-template <int P, bool PQ>
+template <int S, int P, bool PQ>
 struct SlabTab {
-  static constexpr int NB = SlabMI<P, PQ>::NB;
-  double v1[3][P + 1], d1[3][P + 1];
-  __device__ __forceinline__ void load(const BoxConst<3>& b, const double* x) {
+  static constexpr int D = S + 1;
+  static constexpr int NB = SlabMI<S, P, PQ>::NB;
+  double v1[D][P + 1], d1[D][P + 1];
+  __device__ __forceinline__ void load(const BoxConst<D>& b, const double* x) {
 #pragma unroll
-    for (int i = 0; i < 3; ++i) legendre_1d<P>((x[i] - b.c[i]) * b.ih[i], b.rs[i], b.ih[i], v1[i], d1[i]);
+    for (int i = 0; i < D; ++i) legendre_1d<P>((x[i] - b.c[i]) * b.ih[i], b.rs[i], b.ih[i], v1[i], d1[i]);
   }
   __device__ __forceinline__ double val(int f) const {
-    constexpr SlabMI<P, PQ> mi{};
-    return v1[0][mi.a[f][0]] * v1[1][mi.a[f][1]] * v1[2][mi.a[f][2]];
+    constexpr SlabMI<S, P, PQ> mi{};
+    double r = v1[0][mi.a[f][0]];
+#pragma unroll
+    for (int i = 1; i < D; ++i) r *= v1[i][mi.a[f][i]];
+    return r;
   }
   __device__ __forceinline__ double grad(int f, int k) const {
-    constexpr SlabMI<P, PQ> mi{};
+    constexpr SlabMI<S, P, PQ> mi{};
     if (mi.a[f][k] == 0) return 0.0;
-    return (k == 0 ? d1[0][mi.a[f][0]] : v1[0][mi.a[f][0]]) * (k == 1 ? d1[1][mi.a[f][1]] : v1[1][mi.a[f][1]]) *
-           (k == 2 ? d1[2][mi.a[f][2]] : v1[2][mi.a[f][2]]);
+    double r = k == 0 ? d1[0][mi.a[f][0]] : v1[0][mi.a[f][0]];
+#pragma unroll
+    for (int i = 1; i < D; ++i) r *= (k == i ? d1[i][mi.a[f][i]] : v1[i][mi.a[f][i]]);
+    return r;
   }
 };
 
@@ -106,13 +119,14 @@ struct SlabTiles {
 struct SlabArgs {
   pdg_mesh m;       // spatial mesh
   pdg_basis B;      // slab basis: degrees, prism boxes [n][2][3], DoF offsets
-  pdg_rules R;      // spatial triangle rules (vol) + interval rules (face; also the time rules)
+  pdg_rules R;      // spatial rules: simplex (vol) + facet (face)
+  pdg_rules T;      // time rules: interval rules in the face tables
   pdg_params prm;
   pdg_pattern pat;
   pdg_slab sl;
-  const double* sframe;  // spatial simplex frames [n_simplices][8], element order
-  const double* fframe;  // spatial facet frames [n_facets][8]
-  const double* erec;    // spatial basis constants [n_elements][8] (centre, 1/half, 1/sqrt(width))
+  const double* sframe;  // spatial simplex frames [n_simplices][FW], element order (FW = 8 in 2D, 16 in 3D)
+  const double* fframe;  // spatial facet frames [n_facets][FW]
+  const double* erec;    // spatial basis constants [n_elements][FW] (centre, 1/half, 1/sqrt(width))
   const double* sigma;   // lateral penalty per spatial face
   const int8_t* flow;    // lateral flow side per spatial face
   double* values;
@@ -121,8 +135,9 @@ struct SlabArgs {
 };
 
 // shared-memory plan (doubles): table, per-slot scalars, RHS accumulator, neighbour staging
-inline __host__ __device__ int slab_rows(int diff_kind, bool diag, int n_active, bool has_vr, bool has_src) {
-  int vol = diff_kind == PDG_DIFF_NONE ? 0 : (diag ? n_active : 6);
+inline __host__ __device__ int slab_rows(int diff_kind, bool diag, int n_active, bool has_vr, bool has_src,
+                                         int d = 3) {
+  int vol = diff_kind == PDG_DIFF_NONE ? 0 : (diag ? n_active : 2 * d);
   vol += has_vr ? 2 : (has_src ? 1 : 0);
   return vol > 4 ? vol : 4;
 }
@@ -137,37 +152,37 @@ inline __host__ __device__ int slab_table_doubles(int rows, int nbp, int nt, int
   return t > red ? t : red;
 }
 inline __host__ __device__ size_t slab_smem_bytes(int rows, int nbp, int nt, int nw) {
-  // table, per-slot scalars, RHS, neighbour staging (3 doubles + 8 ints per entry)
-  return ((size_t)slab_table_doubles(rows, nbp, nt, nw) + SLAB_NSC * SLAB_KS + nbp + 3 * SLAB_NBR_MAX) * 8 +
+  // table, per-slot scalars, RHS, neighbour staging (4 doubles + 8 ints per entry)
+  return ((size_t)slab_table_doubles(rows, nbp, nt, nw) + SLAB_NSC * SLAB_KS + nbp + 4 * SLAB_NBR_MAX) * 8 +
          (size_t)SLAB_NBR_MAX * 8 * sizeof(int32_t);
 }
 
-template <class CF>
+template <class CF, int D>
 struct SlabRowsOf {
   static constexpr bool DIAG = CF::a_diag();
-  __device__ static constexpr int n_active() {
-    return (CF::a_nz(0, 0) ? 1 : 0) + (CF::a_nz(1, 1) ? 1 : 0) + (CF::a_nz(2, 2) ? 1 : 0);
-  }
   __device__ static constexpr int rowG(int c) {  // table row of the gradient in direction c (diag case)
-    return c == 0 ? 0 : (c == 1 ? (CF::a_nz(0, 0) ? 1 : 0) : (CF::a_nz(0, 0) ? 1 : 0) + (CF::a_nz(1, 1) ? 1 : 0));
+    int r = 0;
+    for (int i = 0; i < c; ++i) r += CF::a_nz(i, i) ? 1 : 0;
+    return r;
   }
+  __device__ static constexpr int n_active() { return rowG(D); }
   __device__ static constexpr int nG() {
-    return CF::diff_kind() == PDG_DIFF_NONE ? 0 : (DIAG ? n_active() : 6);
+    return CF::diff_kind() == PDG_DIFF_NONE ? 0 : (DIAG ? n_active() : 2 * D);
   }
   static constexpr bool HAS_VR = CF::has_adv() || CF::has_reac();
   __device__ static constexpr int rV() { return nG(); }
 };
 
 // flux n.(A grad phi) with the lateral normal (n_s, 0)
-template <int P, bool PQ, class CF>
-__device__ __forceinline__ double slab_flux(const CF& cf, const SlabTab<P, PQ>& tb, int f, const double* n,
+template <int S, int P, bool PQ, class CF>
+__device__ __forceinline__ double slab_flux(const CF& cf, const SlabTab<S, P, PQ>& tb, int f, const double* n,
                                             const double* x) {
   double fl = 0.0;
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < S; ++i) {
     double ag = 0.0;
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
+    for (int j = 0; j <= S; ++j)
       if (CF::a_nz(i, j)) ag += cf.a_ij(i, j, x) * tb.grad(f, j);
     fl += n[i] * ag;
   }
@@ -177,18 +192,20 @@ __device__ __forceinline__ double slab_flux(const CF& cf, const SlabTab<P, PQ>& 
 // prism basis constants: the spatial part from the frame pre-pass records
 // (box_const of the spatial box, pdg_prepass.cu frames_kernel), the time part
 // shared by every prism of the slab
-__device__ __forceinline__ BoxConst<3> slab_box(const double* erec, int64_t e, const BoxConst<1>& tb) {
-  const double* r = erec + e * 8;
-  BoxConst<3> b;
-  b.c[0] = r[0];
-  b.c[1] = r[1];
-  b.ih[0] = r[2];
-  b.ih[1] = r[3];
-  b.rs[0] = r[4];
-  b.rs[1] = r[5];
-  b.c[2] = tb.c[0];
-  b.ih[2] = tb.ih[0];
-  b.rs[2] = tb.rs[0];
+template <int S>
+__device__ __forceinline__ BoxConst<S + 1> slab_box(const double* erec, int64_t e, const BoxConst<1>& tb) {
+  constexpr int FW = S == 2 ? 8 : 16;
+  const double* r = erec + e * FW;
+  BoxConst<S + 1> b;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    b.c[i] = r[i];
+    b.ih[i] = r[S + i];
+    b.rs[i] = r[2 * S + i];
+  }
+  b.c[S] = tb.c[0];
+  b.ih[S] = tb.ih[0];
+  b.rs[S] = tb.rs[0];
   return b;
 }
 
@@ -246,10 +263,13 @@ __device__ __forceinline__ void slab_store(double* values, int64_t voff, int64_t
       }
 }
 
-template <int P, bool PQ, int NW, class CF>
+template <int S, int P, bool PQ, int NW, class CF>
 __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
-  using MI = SlabMI<P, PQ>;
-  using RW = SlabRowsOf<CF>;
+  constexpr int D = S + 1;                 // space-time coordinates, time last
+  constexpr int FW = S == 2 ? 8 : 16;     // spatial frame record width
+  using MI = SlabMI<S, P, PQ>;
+  using RW = SlabRowsOf<CF, D>;
+  using Tab = SlabTab<S, P, PQ>;
   constexpr int NB = MI::NB, NT = (NB + 7) / 8, NBP = NT * 8;
   using TL = SlabTiles<NT, NW>;
   constexpr int WR = TL::WR, WC = TL::WC, WK = TL::WK, TR = TL::TR, TC = TL::TC;
@@ -262,6 +282,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
   const pdg_mesh& m = a.m;
   const pdg_basis& B = a.B;
   const pdg_rules& R = a.R;
+  const pdg_rules& TR_ = a.T;  // time rules (interval rules in the face tables)
   const pdg_pattern& pat = a.pat;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -279,7 +300,8 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
   double* nb_sig = rhs_s + NBP;                                   // [SLAB_NBR_MAX]
   double* nb_n0 = nb_sig + SLAB_NBR_MAX;
   double* nb_n1 = nb_n0 + SLAB_NBR_MAX;
-  int32_t* nb_j = reinterpret_cast<int32_t*>(nb_n1 + SLAB_NBR_MAX);
+  double* nb_n2 = nb_n1 + SLAB_NBR_MAX;
+  int32_t* nb_j = reinterpret_cast<int32_t*>(nb_n2 + SLAB_NBR_MAX);
   int32_t* nb_col = nb_j + SLAB_NBR_MAX;
   int32_t* nb_n = nb_col + SLAB_NBR_MAX;
   int32_t* nb_pj = nb_n + SLAB_NBR_MAX;
@@ -288,12 +310,12 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
   int32_t* nb_info = nb_fb + SLAB_NBR_MAX;
   int32_t* nb_row0 = nb_info + SLAB_NBR_MAX;
   auto TAB = [&](int row, int f, int slot) -> double& { return T[(row * NBP + f) * KSP + slot]; };
-  double* const s0_ = sc;             // volume: w a_00 (diag) / w (full) | face: alpha
-  double* const s1_ = sc + 32;        // w a_11 | beta
-  double* const s2_ = sc + 64;        // w a_22
-  double* const sw_ = sc + 96;        // w (V x R term)
-  double* const r1_ = sc + 128;       // RHS weight of the V row
-  double* const r2_ = sc + 160;       // RHS weight of the F row
+  double* const sca_ = sc;            // volume: w a_cc per direction c (diag) / w (full), rows 0..D-1
+  double* const s0_ = sc;             // face: alpha
+  double* const s1_ = sc + 32;        // face: beta
+  double* const sw_ = sc + 128;       // w (V x R term)
+  double* const r1_ = sc + 160;       // RHS weight of the V row
+  double* const r2_ = sc + 192;       // RHS weight of the F row
   const double t0 = a.sl.t0, tau = a.sl.t1 - a.sl.t0;
   const bool grad_terms = CF::diff_kind() != PDG_DIFF_NONE && a.prm.include_gradient_terms;
   BoxConst<1> tbox;  // time axis of every prism box: (t0, t1)
@@ -307,7 +329,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
     const int pe = B.degree[e];
     const int64_t dof_e = B.dof_offset[e];
     const int ne = (int)(B.dof_offset[e + 1] - dof_e);
-    const BoxConst<3> bx = slab_box(a.erec, e, tbox);
+    const BoxConst<D> bx = slab_box<S>(a.erec, e, tbox);
     const int64_t voff = pat.elem_val_offset[k];
     const int64_t Lrow = pat.row_len[k];
     const int64_t q0 = pat.nbr_ptr[e];
@@ -326,6 +348,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
       nb_sig[q] = rec.sig;
       nb_n0[q] = rec.nrm[0];
       nb_n1[q] = rec.nrm[1];
+      nb_n2[q] = rec.nrm[2];
     }
     for (int f = threadIdx.x; f < NBP; f += NW * 32) rhs_s[f] = 0.0;
     __syncthreads();
@@ -362,7 +385,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
     {
       const int order = 2 * pe + a.prm.quad_increment;
       const int r0s = R.vol_offset[order], nqs = R.vol_count[order];
-      const int r0t = R.face_offset[order], nqt = R.face_count[order];
+      const int r0t = TR_.face_offset[order], nqt = TR_.face_count[order];
       const int nq = nqs * nqt;
       const int64_t s0 = m.elem_ptr[e];
       const int Q = (int)(m.elem_ptr[e + 1] - s0) * nq;
@@ -374,12 +397,12 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
           const int ls = gq / nq;
           const int rem = gq - ls * nq;
           const int is = rem / nqt, it = rem - is * nqt;
-          const double* fr = a.sframe + (s0 + ls) * 8;
-          double x[3];
-          const double det = frame_point<2, 2>(fr, R.points + (r0s + is) * 3, x);
-          x[2] = t0 + tau * R.points[(r0t + it) * 3];
-          const double w = (R.weights[r0s + is] * det) * (tau * R.weights[r0t + it]) * valid;
-          SlabTab<P, PQ> tb;
+          const double* fr = a.sframe + (s0 + ls) * FW;
+          double x[4];
+          const double det = frame_point<S, S>(fr, R.points + (r0s + is) * 3, x);
+          x[S] = t0 + tau * TR_.points[(r0t + it) * 3];
+          const double w = (R.weights[r0s + is] * det) * (tau * TR_.weights[r0t + it]) * valid;
+          Tab tb;
           tb.load(bx, x);
           {
             // this warp's function part (f compile time, the guard warp uniform)
@@ -389,19 +412,19 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
               if (CF::diff_kind() != PDG_DIFF_NONE) {
                 if (RW::DIAG) {
 #pragma unroll
-                  for (int c = 0; c < 3; ++c)
+                  for (int c = 0; c < D; ++c)
                     if (CF::a_nz(c, c)) TAB(RW::rowG(c), f, lane) = f < NB ? tb.grad(f, c) : 0.0;
                 } else {
 #pragma unroll
-                  for (int c = 0; c < 3; ++c) {
+                  for (int c = 0; c < D; ++c) {
                     double ag = 0.0;
                     if (f < NB) {
 #pragma unroll
-                      for (int j = 0; j < 3; ++j)
+                      for (int j = 0; j < D; ++j)
                         if (CF::a_nz(c, j)) ag += cf.a_ij(c, j, x) * tb.grad(f, j);
                     }
                     TAB(c, f, lane) = f < NB ? tb.grad(f, c) : 0.0;
-                    TAB(3 + c, f, lane) = ag;
+                    TAB(D + c, f, lane) = ag;
                   }
                 }
               }
@@ -413,7 +436,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
                   if (f < NB) {
                     if (CF::has_adv()) {
 #pragma unroll
-                      for (int i = 0; i < 3; ++i)
+                      for (int i = 0; i < D; ++i)
                         if (CF::b_nz(i)) rr += cf.b_i(i, x) * tb.grad(f, i);
                     }
                     if (CF::has_reac()) rr += cf.c(x) * vv;
@@ -425,11 +448,11 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
             if (warp == 0) {
               if (CF::diff_kind() != PDG_DIFF_NONE) {
                 if (RW::DIAG) {
-                  if (CF::a_nz(0, 0)) s0_[lane] = w * cf.a_ij(0, 0, x);
-                  if (CF::a_nz(1, 1)) s1_[lane] = w * cf.a_ij(1, 1, x);
-                  if (CF::a_nz(2, 2)) s2_[lane] = w * cf.a_ij(2, 2, x);
+#pragma unroll
+                  for (int c = 0; c < D; ++c)
+                    if (CF::a_nz(c, c)) sca_[c * 32 + lane] = w * cf.a_ij(c, c, x);
                 } else {
-                  s0_[lane] = w;
+                  sca_[lane] = w;
                 }
               }
               sw_[lane] = w;
@@ -444,9 +467,9 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
           if (CF::diff_kind() != PDG_DIFF_NONE) {
             if (RW::DIAG) {
 #pragma unroll
-              for (int c = 0; c < 3; ++c) {
+              for (int c = 0; c < D; ++c) {
                 if (!CF::a_nz(c, c)) continue;
-                const double s = (c == 0 ? s0_ : (c == 1 ? s1_ : s2_))[q];
+                const double s = sca_[c * 32 + q];
                 double lf[TR], rf[TC];
 #pragma unroll
                 for (int i = 0; i < TR; ++i) lf[i] = s * TAB(RW::rowG(c), ((wr * TR + i) % NT) * 8 + g, q);
@@ -459,14 +482,14 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
                     if (wr * TR + i < NT && wc * TC + j < NT) dmma(cd[i][j], lf[i], rf[j]);
               }
             } else {
-              const double s = s0_[q];
+              const double s = sca_[q];
 #pragma unroll
-              for (int c = 0; c < 3; ++c) {
+              for (int c = 0; c < D; ++c) {
                 double lf[TR], rf[TC];
 #pragma unroll
                 for (int i = 0; i < TR; ++i) lf[i] = s * TAB(c, ((wr * TR + i) % NT) * 8 + g, q);
 #pragma unroll
-                for (int j = 0; j < TC; ++j) rf[j] = TAB(3 + c, ((wc * TC + j) % NT) * 8 + g, q);
+                for (int j = 0; j < TC; ++j) rf[j] = TAB(D + c, ((wc * TC + j) % NT) * 8 + g, q);
 #pragma unroll
                 for (int i = 0; i < TR; ++i)
 #pragma unroll
@@ -497,7 +520,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
     // ------------------------------------------------------ face-round helpers
     // Tabulate one lateral / bottom point into rows 0: V_a, 1: F_a (own) and,
     // for interior faces, 2: -V_b, 3: F_b (neighbour); the warp's function part.
-    auto face_tab = [&](const SlabTab<P, PQ>& ta, const SlabTab<P, PQ>& tn, const double* nrm, const double* x,
+    auto face_tab = [&](const Tab& ta, const Tab& tn, const double* nrm, const double* x,
                         bool two, bool useF) {
 #pragma unroll
       for (int f = 0; f < NBP; ++f) {
@@ -505,10 +528,10 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         double va = 0.0, fa = 0.0, vb = 0.0, fb = 0.0;
         if (f < NB) {
           va = ta.val(f);
-          if (useF) fa = slab_flux<P, PQ>(cf, ta, f, nrm, x);
+          if (useF) fa = slab_flux<S, P, PQ>(cf, ta, f, nrm, x);
           if (two) {
             vb = -tn.val(f);
-            if (useF) fb = slab_flux<P, PQ>(cf, tn, f, nrm, x);
+            if (useF) fb = slab_flux<S, P, PQ>(cf, tn, f, nrm, x);
           }
         }
         TAB(0, f, lane) = va;
@@ -576,7 +599,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         if (qb < nnw && nb_j[qb] == e) ++qb;
         auto small = [&](int q) {
           const int o = 2 * max(pe, nb_pj[q]) + a.prm.quad_increment;
-          return (nb_info[q] & 4) && R.face_count[o] <= 4;
+          return (nb_info[q] & 4) && R.face_count[o] * TR_.face_count[o] <= 16;
         };
         if (qb < nnw && small(qn) && small(qb)) {
           {
@@ -584,29 +607,31 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
             const int q = seg ? qb : qn;
             const int o = 2 * max(pe, nb_pj[q]) + a.prm.quad_increment;
             const int r0e = R.face_offset[o], nqe = R.face_count[o];
-            const int nqf = nqe * nqe;
+            const int r0t = TR_.face_offset[o], nqt = TR_.face_count[o];
+            const int nqf = nqe * nqt;
             const double valid = ls < nqf ? 1.0 : 0.0;
             const int gq = min(ls, nqf - 1);
-            const int ie = gq / nqe, it = gq - ie * nqe;
+            const int ie = gq / nqt, it = gq - ie * nqt;
             const int side = nb_info[q] & 1;
             const double sgn = side ? -1.0 : 1.0;
             const bool down = CF::has_adv() && (nb_info[q] & 2) != 0;
-            const double nrm[3] = {nb_n0[q], nb_n1[q], 0.0};
-            double x[3];
+            double nrm[4] = {nb_n0[q], nb_n1[q], S == 3 ? nb_n2[q] : 0.0, 0.0};
+            nrm[S] = 0.0;
+            double x[4];
             const double jac =
-                frame_point<2, 1>(a.fframe + (int64_t)nb_row0[q] * 8, R.points + (r0e + ie) * 3, x);
-            x[2] = t0 + tau * R.points[(r0e + it) * 3];
-            const double w = (R.weights[r0e + ie] * jac) * (tau * R.weights[r0e + it]) * valid;
-            SlabTab<P, PQ> ta, tn;
+                frame_point<S, S - 1>(a.fframe + (int64_t)nb_row0[q] * FW, R.points + (r0e + ie) * 3, x);
+            x[S] = t0 + tau * TR_.points[(r0t + it) * 3];
+            const double w = (R.weights[r0e + ie] * jac) * (tau * TR_.weights[r0t + it]) * valid;
+            Tab ta, tn;
             ta.load(bx, x);
-            tn.load(slab_box(a.erec, nb_j[q], tbox), x);
+            tn.load(slab_box<S>(a.erec, nb_j[q], tbox), x);
             face_tab(ta, tn, nrm, x, true, grad_terms);
             if (warp == 0) {
               double wbn = 0.0;
               if (down) {
                 double bn = 0.0;
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < S; ++i)
                   if (CF::b_nz(i)) bn += cf.b_i(i, x) * nrm[i];
                 wbn = w * bn;
               }
@@ -631,10 +656,11 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         }
       }
       const int pj = nb_pj[qn];
-      const BoxConst<3> bo = slab_box(a.erec, j, tbox);
+      const BoxConst<D> bo = slab_box<S>(a.erec, j, tbox);
       const int order = 2 * max(pe, pj) + a.prm.quad_increment;
       const int r0e = R.face_offset[order], nqe = R.face_count[order];
-      const int nqf = nqe * nqe;  // edge rule x time rule of the same order
+      const int r0t = TR_.face_offset[order], nqt = TR_.face_count[order];
+      const int nqf = nqe * nqt;  // facet rule x time rule of the same order
       double co[TR][TC][2];
       slab_zero<TR, TC>(co);
       for (int32_t f = nb_fa[qn]; f < nb_fb[qn]; ++f) {
@@ -644,8 +670,10 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         const double sgn = side ? -1.0 : 1.0;
         const bool down = CF::has_adv() && (first ? (nb_info[qn] & 2) != 0 : a.flow[f] == side);
         const double sig = first ? nb_sig[qn] : a.sigma[f];
-        double nrm[3] = {first ? nb_n0[qn] : m.face_normal[(int64_t)f * 2],
-                         first ? nb_n1[qn] : m.face_normal[(int64_t)f * 2 + 1], 0.0};
+        double nrm[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < S; ++i)
+          nrm[i] = first ? (i == 0 ? nb_n0[qn] : (i == 1 ? nb_n1[qn] : nb_n2[qn])) : m.face_normal[(int64_t)f * S + i];
         const int64_t row0 = first ? (int64_t)nb_row0[qn] : m.face_ptr[f];
         const int Pf = (int)(m.face_ptr[f + 1] - row0) * nqf;
         for (int base = 0; base < Pf; base += SLAB_KS) {
@@ -655,12 +683,12 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
             const double valid = lane < nvalid ? 1.0 : 0.0;
             const int lr = gq / nqf;
             const int rem = gq - lr * nqf;
-            const int ie = rem / nqe, it = rem - ie * nqe;
-            double x[3];
-            const double jac = frame_point<2, 1>(a.fframe + (row0 + lr) * 8, R.points + (r0e + ie) * 3, x);
-            x[2] = t0 + tau * R.points[(r0e + it) * 3];
-            const double w = (R.weights[r0e + ie] * jac) * (tau * R.weights[r0e + it]) * valid;
-            SlabTab<P, PQ> ta, tn;
+            const int ie = rem / nqt, it = rem - ie * nqt;
+            double x[4];
+            const double jac = frame_point<S, S - 1>(a.fframe + (row0 + lr) * FW, R.points + (r0e + ie) * 3, x);
+            x[S] = t0 + tau * TR_.points[(r0t + it) * 3];
+            const double w = (R.weights[r0e + ie] * jac) * (tau * TR_.weights[r0t + it]) * valid;
+            Tab ta, tn;
             ta.load(bx, x);
             tn.load(bo, x);
             face_tab(ta, tn, nrm, x, true, grad_terms);
@@ -669,7 +697,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
               if (down) {
                 double bn = 0.0;
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < S; ++i)
                   if (CF::b_nz(i)) bn += cf.b_i(i, x) * nrm[i];
                 wbn = w * bn;
               }
@@ -703,8 +731,11 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
       const bool wi = tag == PDG_TAG_DIRICHLET && CF::has_adv() && a.flow[f] == 1;
       const int order = 2 * pe + a.prm.quad_increment;
       const int r0e = R.face_offset[order], nqe = R.face_count[order];
-      const int nqf = nqe * nqe;
-      double nrm[3] = {m.face_normal[(int64_t)f * 2], m.face_normal[(int64_t)f * 2 + 1], 0.0};
+      const int r0t = TR_.face_offset[order], nqt = TR_.face_count[order];
+      const int nqf = nqe * nqt;
+      double nrm[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < S; ++i) nrm[i] = m.face_normal[(int64_t)f * S + i];
       const int64_t row0 = m.face_ptr[f];
       const int Pf = (int)(m.face_ptr[f + 1] - row0) * nqf;
       double dummy[TR][TC][2];
@@ -715,12 +746,12 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
           const double valid = lane < nvalid ? 1.0 : 0.0;
           const int lr = gq / nqf;
           const int rem = gq - lr * nqf;
-          const int ie = rem / nqe, it = rem - ie * nqe;
-          double x[3];
-          const double jac = frame_point<2, 1>(a.fframe + (row0 + lr) * 8, R.points + (r0e + ie) * 3, x);
-          x[2] = t0 + tau * R.points[(r0e + it) * 3];
-          const double w = (R.weights[r0e + ie] * jac) * (tau * R.weights[r0e + it]) * valid;
-          SlabTab<P, PQ> ta;
+          const int ie = rem / nqt, it = rem - ie * nqt;
+          double x[4];
+          const double jac = frame_point<S, S - 1>(a.fframe + (row0 + lr) * FW, R.points + (r0e + ie) * 3, x);
+          x[S] = t0 + tau * TR_.points[(r0t + it) * 3];
+          const double w = (R.weights[r0e + ie] * jac) * (tau * TR_.weights[r0t + it]) * valid;
+          Tab ta;
           ta.load(bx, x);
           face_tab(ta, ta, nrm, x, false, useF);
           if (warp == 0) {
@@ -728,7 +759,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
             if (CF::has_adv() && (wi || tag == PDG_TAG_INFLOW)) {
               double bn = 0.0;
 #pragma unroll
-              for (int i = 0; i < 2; ++i)
+              for (int i = 0; i < S; ++i)
                 if (CF::b_nz(i)) bn += cf.b_i(i, x) * nrm[i];
               wbn = w * bn;
             }
@@ -765,10 +796,10 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
       const int64_t s0 = m.elem_ptr[e];
       const int Q = (int)(m.elem_ptr[e + 1] - s0) * nqs;
       const bool prev = a.sl.prev_values != nullptr;
-      BoxConst<3> bp = bx;
+      BoxConst<D> bp = bx;
       int64_t pdof = 0;
       if (prev) {
-        bp = box_const<3>(a.sl.prev_box + (int64_t)e * 6);
+        bp = box_const<D>(a.sl.prev_box + (int64_t)e * 2 * D);
         pdof = a.sl.prev_dof_offset[e];
       }
       double dummy[TR][TC][2];
@@ -779,20 +810,20 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
           const double valid = lane < nvalid ? 1.0 : 0.0;
           const int ls = gq / nqs;
           const int is = gq - ls * nqs;
-          double x[3];
-          const double det = frame_point<2, 2>(a.sframe + (s0 + ls) * 8, R.points + (r0s + is) * 3, x);
-          x[2] = t0;
+          double x[4];
+          const double det = frame_point<S, S>(a.sframe + (s0 + ls) * FW, R.points + (r0s + is) * 3, x);
+          x[S] = t0;
           const double w = R.weights[r0s + is] * det * valid;
-          SlabTab<P, PQ> ta;
+          Tab ta;
           ta.load(bx, x);
-          const double nrm[3] = {0.0, 0.0, 0.0};
+          const double nrm[4] = {0.0, 0.0, 0.0, 0.0};
           face_tab(ta, ta, nrm, x, false, false);
           if (warp == 0) {
             // b.n with n = (0, 0, -1)
-            const double wbn = CF::b_nz(2) ? -w * cf.b_i(2, x) : 0.0;
+            const double wbn = CF::b_nz(S) ? -w * cf.b_i(S, x) : 0.0;
             double gv;
             if (prev) {
-              SlabTab<P, PQ> tp;
+              Tab tp;
               tp.load(bp, x);
               gv = 0.0;
               const int np_ = (int)(a.sl.prev_dof_offset[e + 1] - pdof);
@@ -839,35 +870,40 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
 // |K| tau / (s+1), prism volume |k| tau, face measure |F| tau, cap p^(2(d-1))
 // with d = 3) and the flow side over the order-2 lateral sample points
 // (spacetime.py:248-263, 287-309).
-template <class CF>
+template <int S, class CF>
 __device__ __forceinline__ void slab_prepass_body(const SlabArgs& a, const CF& cf, double* sigma, int8_t* flow) {
+  constexpr int FW = S == 2 ? 8 : 16;
   const pdg_mesh& m = a.m;
   const pdg_basis& B = a.B;
   const pdg_rules& R = a.R;
+  const pdg_rules& TR_ = a.T;
   const double t0 = a.sl.t0, tau = a.sl.t1 - a.sl.t0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < m.n_faces; f += stride) {
     const int32_t o = m.face_owner[f], nb = m.face_neighbor[f];
     const bool interior = nb >= 0;
     const int tag = interior ? PDG_TAG_INTERIOR : a.sl.lateral_tag[f];
-    const double n[3] = {m.face_normal[f * 2], m.face_normal[f * 2 + 1], 0.0};
+    double n[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < S; ++i) n[i] = m.face_normal[f * S + i];
     sigma[f] = 0.0;
     flow[f] = interior ? -1 : 0;
     if (!interior && tag != PDG_TAG_DIRICHLET) continue;
     if (CF::has_adv()) {
-      const int r0 = R.face_offset[2], nq = R.face_count[2];
+      const int r0 = R.face_offset[2], nq = R.face_count[2];      // facet rule, order 2
+      const int r0t = TR_.face_offset[2], nqt = TR_.face_count[2];  // interval rule, order 2
       double sum = 0.0, mn = PDG_INF, mx = -PDG_INF, amax = 0.0;
       int cnt = 0;
       for (int64_t row = m.face_ptr[f]; row < m.face_ptr[f + 1]; ++row) {
-        const double* fr = a.fframe + row * 8;
+        const double* fr = a.fframe + row * FW;
         for (int i = 0; i < nq; ++i)
-          for (int it = 0; it < nq; ++it) {
-            double x[3];
-            frame_point<2, 1>(fr, R.points + (r0 + i) * 3, x);
-            x[2] = t0 + tau * R.points[(r0 + it) * 3];
+          for (int it = 0; it < nqt; ++it) {
+            double x[4];
+            frame_point<S, S - 1>(fr, R.points + (r0 + i) * 3, x);
+            x[S] = t0 + tau * TR_.points[(r0t + it) * 3];
             double bn = 0.0;
 #pragma unroll
-            for (int k = 0; k < 2; ++k)
+            for (int k = 0; k < S; ++k)
               if (CF::b_nz(k)) bn += cf.b_i(k, x) * n[k];
             sum += bn;
             mn = fmin(mn, bn);
@@ -898,39 +934,42 @@ __device__ __forceinline__ void slab_prepass_body(const SlabArgs& a, const CF& c
         raise_flag(a.flags, PDG_FLAG_NO_ADJACENT_SIMPLEX);
         continue;
       }
-      const double max_adj = mxv * tau / 3.0;
+      const double max_adj = mxv * tau / (double)(S + 1);
       const int p = B.degree[el];
       const double vol = m.elem_volumes[el] * tau;
       double cap = PDG_INF;
-      if (a.prm.coverable && a.prm.coverable[el]) cap = (double)p * p * p * p;
+      if (a.prm.coverable && a.prm.coverable[el]) {  // p^(2(d-1)), d = S + 1
+        cap = 1.0;
+        for (int k = 0; k < 2 * S; ++k) cap *= (double)p;
+      }
       double ab = 0.0;
       if (CF::diff_kind() != PDG_DIFF_NONE) {
         auto nAn = [&](const double* x) {
           double s = 0.0;
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
+          for (int i = 0; i < S; ++i) {
             double r = 0.0;
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < S; ++j)
               if (CF::a_nz(i, j)) r += cf.a_ij(i, j, x) * n[j];
             s += n[i] * r;
           }
           return s;
         };
         if (CF::a_const()) {
-          const double x0[3] = {0.0, 0.0, 0.0};
+          const double x0[4] = {0.0, 0.0, 0.0, 0.0};
           ab = nAn(x0);
         } else {
           const int order = 2 * p + a.prm.quad_increment;
           const int r0s = R.vol_offset[order], nqs = R.vol_count[order];
-          const int r0t = R.face_offset[order], nqt = R.face_count[order];
+          const int r0t = TR_.face_offset[order], nqt = TR_.face_count[order];
           ab = -PDG_INF;
           for (int64_t si = m.elem_ptr[el]; si < m.elem_ptr[el + 1]; ++si)
             for (int is = 0; is < nqs; ++is)
               for (int it = 0; it < nqt; ++it) {
-                double x[3];
-                frame_point<2, 2>(a.sframe + si * 8, R.points + (r0s + is) * 3, x);
-                x[2] = t0 + tau * R.points[(r0t + it) * 3];
+                double x[4];
+                frame_point<S, S>(a.sframe + si * FW, R.points + (r0s + is) * 3, x);
+                x[S] = t0 + tau * TR_.points[(r0t + it) * 3];
                 ab = fmax(ab, nAn(x));
               }
         }

@@ -531,12 +531,12 @@ def policy_source(coeffs, dim: int, initial=None) -> str:
     return _policy(coeffs, dim, initial)[0]
 
 
-def slab_policy(coeffs, initial=None, with_info=False):
+def slab_policy(coeffs, initial=None, with_info=False, dim=3):
     """(policy source, shared-memory table rows[, info]) of a space-time slab
     (coordinates (x, y, t)); the rows follow ``slab_rows`` in slab_body.cuh."""
-    src, info = _policy(coeffs, 3, initial, sinpi=False)
+    src, info = _policy(coeffs, dim, initial, sinpi=False)
     kind, diag, n_act = info["kind"], info["diag"], info["n_active"]
-    vol = 0 if kind == 0 else (n_act if diag else 6)
+    vol = 0 if kind == 0 else (n_act if diag else 2 * dim)
     has_vr = info["adv"] or info["reac"]
     vol += 2 if has_vr else (1 if info["src"] else 0)
     return (src, max(vol, 4), info) if with_info else (src, max(vol, 4))

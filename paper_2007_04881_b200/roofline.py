@@ -88,11 +88,12 @@ def slab_work(plan) -> dict:
     owned = np.zeros(f.n_elements, bool)
     owned[plan.row_elements] = True
     info = plan.policy_info
-    items = (info["n_active"] if info["diag"] else 3) * (info["kind"] != 0) + int(info["adv"]) + int(info["reac"])
+    S = f.dim
+    items = (info["n_active"] if info["diag"] else S + 1) * (info["kind"] != 0) + int(info["adv"]) + int(info["reac"])
     nsim = np.diff(f.elem_ptr).astype(np.float64)
     m = ((2 * deg + inc + 2) // 2).astype(np.float64)
-    vol = float(np.sum((nsim * 2.0 * n * n * m ** 3 * items)[owned]))
-    bottom = float(np.sum((nsim * 2.0 * n * n * m ** 2)[owned])) if info["adv"] else 0.0
+    vol = float(np.sum((nsim * 2.0 * n * n * m ** (S + 1) * items)[owned]))
+    bottom = float(np.sum((nsim * 2.0 * n * n * m ** S)[owned])) if info["adv"] else 0.0
     nfac = np.diff(f.face_ptr).astype(np.float64)
     o, nbh = f.face_owner, f.face_neighbor
     inter = nbh != BOUNDARY
@@ -102,10 +103,10 @@ def slab_work(plan) -> dict:
     nmax = np.where(inter, np.maximum(n[o], n[nbs]), n[o])
     sides = owned[o].astype(np.float64) + np.where(inter, owned[nbs], False).astype(np.float64)
     up = 4.0 * float(info["adv_spatial"])
-    face_int = float(np.sum(((16.0 + up) * nmax ** 2 * mf ** 2 * nfac * sides / 2.0)[inter]))
+    face_int = float(np.sum(((16.0 + up) * nmax ** 2 * mf ** S * nfac * sides / 2.0)[inter]))
     tag = plan.lateral_tags
     dirich = (~inter) & (tag == TAG_CODE["dirichlet"]) & owned[o]
-    face_d = float(np.sum((4.0 * n[o] ** 2 * mf ** 2 * nfac)[dirich]))
+    face_d = float(np.sum((4.0 * n[o] ** 2 * mf ** S * nfac)[dirich]))
     flops = vol + bottom + face_int + face_d
     nnz = float(plan.nnz)
     geo = float(np.sum(nsim[owned])) * 8.0 * 6 + float(np.sum(nfac[inter | owned[o]])) * 40.0

@@ -145,13 +145,14 @@ def classify_lateral_faces(flat, t0, t1, coeffs, dirichlet_predicate=None) -> np
     tau = t1 - t0
     tp = t0 + tau * tr.points[:, 0]
     nt = tp.shape[0]
-    pts = np.empty((sp.shape[0] * nt, 3))
-    pts[:, :2] = np.repeat(sp, nt, axis=0)
-    pts[:, 2] = np.tile(tp, sp.shape[0])
+    S = flat.dim
+    pts = np.empty((sp.shape[0] * nt, S + 1))
+    pts[:, :S] = np.repeat(sp, nt, axis=0)
+    pts[:, S] = np.tile(tp, sp.shape[0])
     which = np.repeat(which, nt)
     counts = counts * nt
-    n3 = np.zeros((bf.size, 3))
-    n3[:, :2] = flat.face_normal[bf]
+    n3 = np.zeros((bf.size, S + 1))
+    n3[:, :S] = flat.face_normal[bf]
     mean = np.add.reduceat(pts, np.r_[0, np.cumsum(counts)[:-1]], axis=0) / counts[:, None]
     out = np.full(bf.size, tag_code(BoundaryTag.OUTFLOW), np.int8)
     decided = np.zeros(bf.size, bool)
@@ -203,15 +204,17 @@ class SlabPlan:
         self.dm = device_mesh(slab.spatial, device)
         dev = self.device = self.dm.device
         flat = self.flat = self.dm.flat
-        if flat.dim != 2:
-            raise NotImplementedError("the device slab engine supports 2D spatial meshes (3D prisms)")
+        if flat.dim not in (2, 3):
+            raise NotImplementedError("the device slab engine supports 2D and 3D spatial meshes")
+        S = flat.dim
+        self.S = S
         deg, boxes, fam = spec_arrays(specs)
         fname = family_name(fam)
         if deg.shape[0] != flat.n_elements:
             raise AssemblyError("one BasisSpec per element required")
-        if boxes.shape[1:] != (2, 3):
-            raise ValueError("slab spec boxes must be (2, 3): spatial box x interval")
-        if not (np.all(boxes[:, 0, 2] == slab.t0) and np.all(boxes[:, 1, 2] == slab.t1)):
+        if boxes.shape[1:] != (2, S + 1):
+            raise ValueError(f"slab spec boxes must be (2, {S + 1}): spatial box x interval")
+        if not (np.all(boxes[:, 0, S] == slab.t0) and np.all(boxes[:, 1, S] == slab.t1)):
             raise NotImplementedError("the device slab engine needs prism boxes with the slab's time "
                                       "interval (build_slab)")
         pmax = int(deg.max()) if deg.size else 0
@@ -220,7 +223,7 @@ class SlabPlan:
                                       f"(p <= {_lib.SLAB_MAX_DEGREE[fname]} for family {fname})")
         if fname == "PQ" and np.any(deg != pmax):
             raise NotImplementedError("family PQ slabs need a uniform degree on the device")
-        counts = np.array([num_basis(int(p), 3, fam) for p in deg], np.int64)
+        counts = np.array([num_basis(int(p), S + 1, fam) for p in deg], np.int64)
         self.dof = DofMap(np.concatenate([[0], np.cumsum(counts)]).astype(np.int64))
         self.degrees = deg
         inc = int(config.quad_increment)
@@ -228,7 +231,7 @@ class SlabPlan:
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
         self.t = {"degree": T(deg.astype(np.int32)), "box": T(boxes), "dof": T(self.dof.offsets),
-                  "sbox": T(np.ascontiguousarray(boxes[:, :, :2]))}
+                  "sbox": T(np.ascontiguousarray(boxes[:, :, :S]))}
         b = _lib.Basis()
         b.max_degree = pmax
         b.degree, b.box, b.dof_offset = _lib.ptr(self.t["degree"]), _lib.ptr(self.t["box"]), _lib.ptr(self.t["dof"])
@@ -241,7 +244,9 @@ class SlabPlan:
         uniq = np.unique(deg)
         vol_orders = [2 * int(p) + inc for p in uniq]
         face_orders = [2 * int(max(p, q)) + inc for p in uniq for q in uniq] + vol_orders
-        self.rules = DeviceRules(2, vol_orders, face_orders, dev)
+        self.rules = DeviceRules(S, vol_orders, face_orders, dev)
+        # time axis: interval rules of every order in use (face tables of a 1D-facet table)
+        self.trules = DeviceRules(2, [], sorted(set(face_orders) | {2}), dev)
 
         # time-jump data (spacetime.py:367-388)
         initial = None
@@ -254,7 +259,7 @@ class SlabPlan:
             pspecs, pvec = u_prev
             pdeg, pbox, pfam = spec_arrays(pspecs)
             pvec = np.asarray(pvec, dtype=np.float64)
-            pcounts = np.array([num_basis(int(p), 3, pfam) for p in pdeg], np.int64)
+            pcounts = np.array([num_basis(int(p), S + 1, pfam) for p in pdeg], np.int64)
             if pcounts.sum() != pvec.shape[0]:
                 raise MeshError(f"previous solution has {pvec.shape[0]} dofs, expected {int(pcounts.sum())}")
             if pdeg.shape[0] != flat.n_elements:
@@ -264,10 +269,10 @@ class SlabPlan:
             self.t["prev"] = T(pvec)
             self.t["prev_dof"] = T(np.concatenate([[0], np.cumsum(pcounts)]).astype(np.int64))
             self.t["prev_box"] = T(pbox)
-        self.policy, rows, self.policy_info = slab_policy(coeffs, initial, with_info=True)
+        self.policy, rows, self.policy_info = slab_policy(coeffs, initial, with_info=True, dim=S + 1)
         self.family = fam
         self.policy = self.policy.encode()
-        _lib.check(self.lib.pdg_slab_prepare(self.policy, pmax, 1 if fname == "PQ" else 0))
+        _lib.check(self.lib.pdg_slab_prepare(self.policy, S, pmax, 1 if fname == "PQ" else 0))
 
         tags = classify_lateral_faces(flat, slab.t0, slab.t1, coeffs, dirichlet_predicate)
         self.lateral_tags = tags
@@ -280,6 +285,7 @@ class SlabPlan:
         s.prev_box = _lib.ptr(self.t["prev_box"])
         s.family = 1 if fname == "PQ" else 0
         s.table_rows = rows
+        s.time_rules = self.trules.struct
         self.sdesc = s
 
         prm = _lib.Params()
@@ -300,6 +306,7 @@ class SlabPlan:
             self.t["rows"] = T(self.row_elements.astype(np.int32))
         nr = self.row_elements.shape[0]
         self.n_local_rows = int(counts[self.row_elements].sum())
+        FW = 8 if S == 2 else 16
         z = lambda n, dt: torch.empty(max(int(n), 1), dtype=dt, device=dev)
         i64, i32 = torch.int64, torch.int32
         nadj = nel + 2 * flat.n_interfaces
@@ -309,8 +316,8 @@ class SlabPlan:
                       nbr_rec=z(nadj * 10, torch.float64),  # pdg_iface_rec, 80 B per entry
                       sigma=z(flat.n_faces, torch.float64), flow=z(flat.n_faces, torch.int8),
                       flags=torch.zeros(1, dtype=torch.int32, device=dev),
-                      sframe=z(flat.n_simplices * 8, torch.float64), fframe=z(flat.n_facets * 8, torch.float64),
-                      erec=z(nel * 8, torch.float64))
+                      sframe=z(flat.n_simplices * FW, torch.float64), fframe=z(flat.n_facets * FW, torch.float64),
+                      erec=z(nel * FW, torch.float64))
         fr = _lib.Frames()
         fr.simplex, fr.facet, fr.element = _lib.ptr(self.t["sframe"]), _lib.ptr(self.t["fframe"]), _lib.ptr(self.t["erec"])
         self.frames = fr

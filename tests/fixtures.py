@@ -237,3 +237,17 @@ def slab_predicate(name):
     if name == "slab_adv_heat":
         return lambda p: bool(p[0] < 0.5)
     return None
+
+
+def slab_heat3d():
+    """3+1D heat problem (spacetime over a 3D mesh): u = sin sin sin (1 - t)."""
+    pi = np.pi
+    W = M.coord(3)
+    s = M.sin(pi * X) * M.sin(pi * Y) * M.sin(pi * Z)
+    coeffs = M.PdeCoefficients(
+        diffusion=M.constant_tensor(np.diag([1.0, 1.0, 1.0, 0.0])),
+        advection=M.constant_vector([0.0, 0.0, 0.0, 1.0]),
+        reaction=M.constant_scalar(1.0),
+        source=M.ScalarField(s * ((3.0 * pi ** 2 + 1.0) * (1.0 - W) - 1.0)),
+        dirichlet_data=M.ScalarField(s * (1.0 - W)))
+    return coeffs, M.ScalarField(s)

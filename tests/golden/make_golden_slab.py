@@ -56,6 +56,18 @@ def ref_slab_coeffs(name):
                                dirichlet_data=lambda p: p[:, 0] + p[:, 2],
                                neumann_data=lambda p: 1.0 + p[:, 1])
         return C, lambda xy: xy[:, 0] * xy[:, 1]
+    if name == "slab_heat3d":
+        def u(p):
+            return np.sin(pi * p[:, 0]) * np.sin(pi * p[:, 1]) * np.sin(pi * p[:, 2]) * (1.0 - p[:, 3])
+
+        def f(p):
+            s = np.sin(pi * p[:, 0]) * np.sin(pi * p[:, 1]) * np.sin(pi * p[:, 2])
+            return s * ((3.0 * pi ** 2 + 1.0) * (1.0 - p[:, 3]) - 1.0)
+
+        C = Rm.PdeCoefficients(diffusion=Rm.constant_tensor(np.diag([1.0, 1.0, 1.0, 0.0])),
+                               advection=Rm.constant_vector([0.0, 0.0, 0.0, 1.0]),
+                               reaction=Rm.constant_scalar(1.0), source=f, dirichlet_data=u)
+        return C, lambda x: np.sin(pi * x[:, 0]) * np.sin(pi * x[:, 1]) * np.sin(pi * x[:, 2])
     if name == "slab_transport":
         C = Rm.PdeCoefficients(advection=Rm.constant_vector([1.0, 0.5, 1.0]),
                                reaction=Rm.constant_scalar(0.5),
@@ -82,6 +94,9 @@ def cases():
         ("slab_transport_p2_prev", g10, c10, (0.5, 1.0), 2, "P", "slab_transport", (0.0, 0.5, 12)),
         ("slab_heat_pq3", g6, F.grown_clusters(g6, 7, seed=1), (0.0, 0.2), 3, "PQ", "slab_heat", None),
         ("slab_advheat_p1", g10, c10, (0.0, 0.1), 1, "P", "slab_adv_heat", None),
+        ("slab_3d_heat_pq1", F.cube_grid(2), F.cube_blocks(2, 1), (0.0, 0.2), 1, "PQ", "slab_heat3d", None),
+        ("slab_3d_heat_p2_prev", F.cube_grid(2), F.grown_clusters(F.cube_grid(2), 5, seed=1), (0.2, 0.4), 2, "P",
+         "slab_heat3d", (0.0, 0.2, 13)),
     ]
 
 

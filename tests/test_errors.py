@@ -47,10 +47,6 @@ def test_slab_unsupported_inputs():
     from paper_2007_04881_b200.spacetime import assemble_slab, build_slab
 
     coeffs, initial = F.slab_heat()
-    pm3 = agglomerate(F.cube_grid(2), F.cube_blocks(2, 1))
-    slab, specs = build_slab(pm3, (0.0, 0.1), 1, Family.PQ)
-    with pytest.raises(NotImplementedError):
-        assemble_slab(slab, coeffs, specs, initial)
     pm = agglomerate(F.square_grid(4), F.square_blocks(4, 2))
     slab, specs = build_slab(pm, (0.0, 0.1), np.array([1, 2, 1, 1]), Family.PQ)
     with pytest.raises(NotImplementedError):  # PQ needs a uniform degree on the device

@@ -22,7 +22,7 @@ GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "sla
 
 def load_slab_case(path):
     z = np.load(path, allow_pickle=False)
-    base = SimplicialMesh(2, z["vertices"], z["simplices"])
+    base = SimplicialMesh(int(z["vertices"].shape[1]), z["vertices"], z["simplices"])
     pm = agglomerate(base, z["agg"])
     cname = str(z["coeffs"])
     coeffs, initial = getattr(F, cname)()
@@ -56,7 +56,7 @@ def test_slab_oracle_reproduces_reference_golden(path):
 
 
 def test_slab_golden_set_present():
-    assert len(GOLDEN) >= 6
+    assert len(GOLDEN) >= 8  # 6 over 2D meshes, 2 over 3D meshes (3+1D prisms)
 
 
 def test_time_partition_validation():

@@ -18,10 +18,10 @@ def main(case="slab_heat", degree="2", fam="PQ", nw="4"):
     src = ('#include "slab_body.cuh"\nnamespace pdg_jit {\nusing namespace pdg;\n' + pol + '\n}\n'
            f'extern "C" __global__ void __launch_bounds__({32 * int(nw)}, 1) '
            'pdg_slab_kernel(const __grid_constant__ pdg::SlabArgs a) {\n'
-           f'  pdg::slab_body<{degree}, {pq}, {nw}, pdg_jit::JitCoef>(a, pdg_jit::JitCoef());\n}}\n'
+           f'  pdg::slab_body<2, {degree}, {pq}, {nw}, pdg_jit::JitCoef>(a, pdg_jit::JitCoef());\n}}\n'
            'extern "C" __global__ void __launch_bounds__(128) '
            'pdg_slab_prepass(const __grid_constant__ pdg::SlabArgs a, double* sigma, int8_t* flow) {\n'
-           '  pdg::slab_prepass_body(a, pdg_jit::JitCoef(), sigma, flow);\n}\n')
+           '  pdg::slab_prepass_body<2>(a, pdg_jit::JitCoef(), sigma, flow);\n}\n')
     lib = C.CDLL("libnvrtc.so.12")
     prog = C.c_void_p()
     assert lib.nvrtcCreateProgram(C.byref(prog), src.encode(), b"pdg_jit.cu", 0, None, None) == 0
