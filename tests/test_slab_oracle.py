@@ -188,3 +188,19 @@ def test_march_two_slabs_against_oracle():
     assert_parity(m, rhs, ref, _offsets(specs2))
     # the discrete solution approximates u = sin sin (1 - t) at the slab end
     assert np.all(np.isfinite(sols[1]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,fam", [(0, "PQ"), (1, "PQ"), (2, "PQ"), (1, "P"), (2, "P"), (3, "P")])
+def test_slab_engine_3d_spatial_against_oracle(p, fam):
+    """3+1D prisms (spacetime over a 3D agglomerated mesh; polydg
+    test_spacetime.py:278-290 exercises this dimension at p = 0)."""
+    from paper_2007_04881_b200.spacetime import assemble_slab
+
+    g = F.cube_grid(3)
+    pm = agglomerate(g, F.grown_clusters(g, 9, seed=4))
+    coeffs, initial = F.slab_heat3d()
+    slab, specs = build_slab(pm, (0.1, 0.3), p, Family(fam))
+    m, rhs, _ = assemble_slab(slab, coeffs, specs, initial)
+    ref = OS.assemble_slab(pm, 0.1, 0.3, coeffs, specs, initial)
+    assert_parity(m, rhs, ref, _offsets(specs))
