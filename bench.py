@@ -332,6 +332,16 @@ def run_ours(args, w, rank, world, local_rank):
         plan.run()
     plan.check_flags()
 
+    # CUDA graphs: a step = 3 graph launches (index, pre-pass, element kernel)
+    # instead of ~20 kernel launches -- small meshes are launch-bound
+    graphs = (os.environ.get("PDG_GRAPHS", "1") != "0" and hasattr(plan, "capture_graphs")
+              and plan.capture_graphs())
+    step = plan.run_graphs if graphs else plan.run
+    if graphs:
+        for _ in range(2):
+            step()
+        plan.check_flags()
+
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     t_start = torch.cuda.Event(enable_timing=True)
@@ -343,12 +353,12 @@ def run_ours(args, w, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         t_start.record(stream)
         for k in range(K):
-            plan.run(evs[k])
+            step(evs[k])
         t_stop.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    launches = int(lib.pdg_launch_count() - l0)
+    launches = int(lib.pdg_launch_count() - l0) + (plan.graph_launches * K if graphs else 0)
     ms = t_start.elapsed_time(t_stop) / K
     ms_index = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     ms_pre = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
@@ -362,7 +372,7 @@ def run_ours(args, w, rank, world, local_rank):
     if not args.no_e2e and not args.profile and args.e2e_steps > 0:
         io = HostIO(plan)
         h2d, d2h = io.h2d_bytes, io.d2h_bytes
-        io.upload(); plan.run(); io.download()
+        io.upload(); step(); io.download()
         stream.synchronize()
         if world > 1:
             dist.barrier()
@@ -372,7 +382,7 @@ def run_ours(args, w, rank, world, local_rank):
         e0.record(stream)
         for _ in range(args.e2e_steps):
             io.upload()
-            plan.run()
+            step()
             io.download()
         e1.record(stream)
         stream.synchronize()
@@ -433,6 +443,7 @@ def run_ours(args, w, rank, world, local_rank):
                      "peak_source": peak_src},
         "clocks": clk.summary(),
         "gpu_launches": int(round(launches_tot * K)),
+        "cuda_graphs": bool(graphs),
         "gpu_launches_per_step": launches_tot,
     }
     if slab_case:

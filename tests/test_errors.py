@@ -68,3 +68,27 @@ def test_no_cpu_fallback_without_a_gpu(monkeypatch):
     classify_boundary_faces(pm, C)
     with pytest.raises(_lib.EngineUnavailable):
         assemble_approach2(pm, C, build_basis(pm, 1))
+
+
+@pytest.mark.gpu
+def test_cuda_graph_replay_bitwise_equal_to_plain_launches():
+    """The bench's CUDA-graph step (3 graph launches) reproduces the plain
+    launches bit for bit."""
+    from paper_2007_04881_b200.assembly import SipgPlan
+
+    pm = agglomerate(F.square_grid(10), F.grown_clusters(F.square_grid(10), 23, seed=2))
+    C = F.adr(2)
+    classify_boundary_faces(pm, C)
+    plan = SipgPlan(pm, C, build_basis(pm, 3))
+    plan.run()
+    plan.check_flags()
+    v0, r0, c0 = plan.values.clone(), plan.rhs.clone(), plan.col_idx.clone()
+    assert plan.capture_graphs()
+    plan.t["values"].zero_()
+    plan.t["rhs"].zero_()
+    plan.t["col_idx"].zero_()
+    for _ in range(3):
+        plan.run_graphs()
+    plan.check_flags()
+    assert plan.graph_launches > 0
+    assert bool((plan.values == v0).all()) and bool((plan.rhs == r0).all()) and bool((plan.col_idx == c0).all())
