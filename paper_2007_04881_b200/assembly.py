@@ -573,6 +573,10 @@ class SipgPlan:
         if getattr(self, "graphs", None):
             return True
         try:
+            if self.stream.cuda_stream == torch.cuda.default_stream(self.device).cuda_stream:
+                # graphs are captured on a side stream (replays stay ordered on it)
+                torch.cuda.synchronize(self.device)
+                self.stream = torch.cuda.Stream(self.device)
             self.run()  # warm: JIT compile / function attributes outside the capture
             self.stream.synchronize()
             l0 = self.lib.pdg_launch_count()
