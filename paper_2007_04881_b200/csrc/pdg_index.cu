@@ -146,10 +146,44 @@ __global__ void adj_fill_ifaces(const pdg_mesh m, int32_t* elem, int32_t* ifc, i
 
 // insertion sort of each (short) neighbour segment by element id: the atomic
 // fill order is arbitrary, the sorted result is unique (ids are distinct).
+// Segments up to ADJ_REG entries are sorted in registers (fully unrolled
+// compare-exchange passes, one global read + one write per entry); longer
+// ones fall back to the in-place insertion sort.
+constexpr int ADJ_REG = 16;
 __global__ void adj_sort(const pdg_mesh m, const int64_t* ptr, int32_t* elem, int32_t* ifc) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m.n_elements; e += stride) {
     const int64_t a = ptr[e], b = ptr[e + 1];
+    const int n = (int)(b - a);
+    if (n <= ADJ_REG) {
+      int32_t ke[ADJ_REG], ki[ADJ_REG];
+#pragma unroll
+      for (int i = 0; i < ADJ_REG; ++i) {
+        ke[i] = i < n ? elem[a + i] : 0x7fffffff;
+        ki[i] = i < n ? ifc[a + i] : 0;
+      }
+      // odd-even transposition sort (ADJ_REG passes, all indices compile time)
+#pragma unroll
+      for (int pass = 0; pass < ADJ_REG; ++pass) {
+#pragma unroll
+        for (int i = pass & 1; i + 1 < ADJ_REG; i += 2) {
+          const bool sw = ke[i] > ke[i + 1];
+          const int32_t k0 = sw ? ke[i + 1] : ke[i], k1 = sw ? ke[i] : ke[i + 1];
+          const int32_t i0 = sw ? ki[i + 1] : ki[i], i1 = sw ? ki[i] : ki[i + 1];
+          ke[i] = k0;
+          ke[i + 1] = k1;
+          ki[i] = i0;
+          ki[i + 1] = i1;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < ADJ_REG; ++i)
+        if (i < n) {
+          elem[a + i] = ke[i];
+          ifc[a + i] = ki[i];
+        }
+      continue;
+    }
     for (int64_t i = a + 1; i < b; ++i) {
       const int32_t ke = elem[i], ki = ifc[i];
       int64_t j = i - 1;
@@ -182,13 +216,32 @@ __global__ void pattern_counts(const pdg_basis B, const pdg_pattern P, int64_t* 
   }
 }
 
+// row_ptr of the owned rows: one warp per 32 consecutive row elements, lanes
+// over the rows of that range (contiguous, coalesced stores), the row's
+// element found by a binary search over the 32 staged row offsets.
 __global__ void pattern_row_ptr(const pdg_basis B, const pdg_pattern P) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < P.n_row_elements; k += stride) {
-    const int64_t r0 = P.elem_row_offset[k], r1 = P.elem_row_offset[k + 1];
-    const int64_t v0 = P.elem_val_offset[k], L = P.row_len[k];
-    for (int64_t r = r0; r < r1; ++r) P.row_ptr[r] = v0 + (r - r0) * L;
-    if (k == P.n_row_elements - 1) P.row_ptr[r1] = P.elem_val_offset[k + 1];
+  __shared__ int64_t sro[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; k0 < P.n_row_elements;
+       k0 += nw * 32) {
+    const int cnt = (int)(P.n_row_elements - k0 < 32 ? P.n_row_elements - k0 : 32);
+    if (lane < cnt) sro[w][lane] = P.elem_row_offset[k0 + lane];
+    if (lane == 0) sro[w][cnt] = P.elem_row_offset[k0 + cnt];
+    __syncwarp();
+    const int64_t R0 = sro[w][0], R1 = sro[w][cnt];
+    for (int64_t r = R0 + lane; r < R1; r += 32) {
+      int lo = 0, hi = cnt - 1;  // last element with row offset <= r
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sro[w][mid] <= r) lo = mid;
+        else hi = mid - 1;
+      }
+      const int64_t k = k0 + lo;
+      P.row_ptr[r] = P.elem_val_offset[k] + (r - sro[w][lo]) * P.row_len[k];
+    }
+    if (lane == 0 && k0 + cnt == P.n_row_elements) P.row_ptr[R1] = P.elem_val_offset[P.n_row_elements];
+    __syncwarp();
   }
 }
 
@@ -257,7 +310,10 @@ extern "C" int pdg_pattern_offsets(const pdg_mesh* mesh, const pdg_basis* basis,
     pattern_counts<<<grid_for(nr), 256, 0, st>>>(*basis, *pattern, vals, rows); note_launch();
     PDG_CUDA(exclusive_scan(vals, nr, pattern->elem_val_offset, scan_ws, st));
     PDG_CUDA(exclusive_scan(rows, nr, pattern->elem_row_offset, scan_ws, st));
-    if (nr > 0) { pattern_row_ptr<<<grid_for(nr), 256, 0, st>>>(*basis, *pattern); note_launch(); }
+    if (nr > 0) {
+      pattern_row_ptr<<<grid_for_warps((nr + 31) / 32, 256), 256, 0, st>>>(*basis, *pattern);
+      note_launch();
+    }
     else PDG_CUDA(cudaMemsetAsync(pattern->row_ptr, 0, sizeof(int64_t), st));
     PDG_CUDA(cudaGetLastError());
     if (nnz_host) {  // size query: one synchronisation to size col_idx / values
