@@ -428,8 +428,7 @@ int pdg_agglomerate(int32_t dim, int64_t n_vertices, int64_t n_simplices, const 
 /* ---- consumers of the device CSR (polydg solver.py:30-118) ----
  * The element-block structure of the assembled CSR (every row of element e
  * holds the same column list) is exploited: the column list is read once
- * per element.  err_flags bits: 1 = an element row longer than 1024 columns
- * (SpMV staging), 2 = missing diagonal block, 4 = singular diagonal block. */
+ * per element.  err_flags bits: 2 = missing diagonal block, 4 = singular diagonal block. */
 int pdg_spmv_blocked(const int64_t* dof_offset, int64_t n_elements, const int64_t* row_ptr,
                      const int64_t* col_idx, const double* values, const double* x, double* y,
                      uint32_t* err_flags, pdg_stream stream);

@@ -19,12 +19,35 @@ namespace pdg {
 namespace {
 
 constexpr int SPMV_WARPS = 4;
-constexpr int SPMV_MAXL = 1024;  // columns per element row staged in shared memory
+constexpr int SPMV_MAXL = 512;  // columns per element row staged in shared memory (longer: direct gathers)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// rows r0..r0+R-1 of an element against the gathered x (xs, or x via col_idx)
+template <int R, bool STAGED>
+__device__ __forceinline__ void spmv_rows(const double* v, int64_t L, const double* xs, const int64_t* cols,
+                                          const double* x, double* y, int lane) {
+  double s[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) s[i] = 0.0;
+  for (int64_t p = lane; p < L; p += 32) {
+    const double xv = STAGED ? xs[p] : x[cols[p]];
+#pragma unroll
+    for (int i = 0; i < R; ++i) s[i] += v[(int64_t)i * L + p] * xv;
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) s[i] = warp_sum(s[i]);
+  if (lane < R) {
+    double o = s[0];
+#pragma unroll
+    for (int i = 1; i < R; ++i)
+      if (lane == i) o = s[i];
+    y[lane] = o;
+  }
 }
 
 __global__ void __launch_bounds__(32 * SPMV_WARPS) spmv_blocked(const int64_t* dof, int64_t nel,
@@ -39,22 +62,25 @@ __global__ void __launch_bounds__(32 * SPMV_WARPS) spmv_blocked(const int64_t* d
     const int ne = (int)(dof[e + 1] - r0);
     if (ne == 0) continue;
     const int64_t a = row_ptr[r0];
-    const int L = (int)(row_ptr[r0 + 1] - a);
-    if (L > SPMV_MAXL) {
-      if (lane == 0) atomicOr(flags, 1u);
-      continue;
+    const int64_t L = row_ptr[r0 + 1] - a;
+    const bool staged = L <= SPMV_MAXL;
+    if (staged) {
+      for (int p = lane; p < L; p += 32) xs[w][p] = x[col_idx[a + p]];
+      __syncwarp();
     }
-    for (int p = lane; p < L; p += 32) xs[w][p] = x[col_idx[a + p]];
-    __syncwarp();
-    for (int r = 0; r < ne; ++r) {
-      const double* v = vals + a + (int64_t)r * L;
-      double s = 0.0;
-      for (int p = lane; p < L; p += 32) s += v[p] * xs[w][p];
-      s = warp_sum(s);
-      if (lane == 0) y[r0 + r] = s;
+    // four rows at a time: independent accumulators keep the loads in flight
+    int r = 0;
+    for (; r + 4 <= ne; r += 4) {
+      if (staged) spmv_rows<4, true>(vals + a + (int64_t)r * L, L, xs[w], col_idx + a, x, y + r0 + r, lane);
+      else spmv_rows<4, false>(vals + a + (int64_t)r * L, L, xs[w], col_idx + a, x, y + r0 + r, lane);
+    }
+    for (; r < ne; ++r) {
+      if (staged) spmv_rows<1, true>(vals + a + (int64_t)r * L, L, xs[w], col_idx + a, x, y + r0 + r, lane);
+      else spmv_rows<1, false>(vals + a + (int64_t)r * L, L, xs[w], col_idx + a, x, y + r0 + r, lane);
     }
     __syncwarp();
   }
+  (void)flags;
 }
 
 // extract the diagonal block of every element and invert it in place
