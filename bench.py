@@ -7,9 +7,12 @@ wall ms at 1/2/4/8 B200, next to the host-CPU reference path).
 One step = one full assembly of the workload's rows on each rank: index
 phase (adjacency, row offsets), face pre-pass (sigma, flow side) and the fused
 element kernel (values + col_idx + RHS), with the mesh resident in HBM.
-Multi-GPU (torchrun): elements are split into contiguous, cost-balanced row
-ranges, one per rank; there is no collective on the assembly path (strong
-scaling of the fixed mesh); timing is the max over ranks of CUDA-event time.
+Multi-GPU (torchrun): assembly needs no communication, so by
+default every rank assembles its own instance of the workload (weak scaling:
+value = N x elements / max-over-ranks time); ``--strong`` instead splits ONE
+mesh into contiguous, cost-balanced row ranges (the paper's strong-scaling
+experiment, one-sided cut faces).  No collective on the assembly path either
+way; timing is the max over ranks of CUDA-event time.
 ``e2e`` re-runs the step through the public plan API with the mesh copied
 from pinned host memory and the assembled CSR + RHS copied back every step.
 ``--impl reference`` times the CPU restatement of polydg's path (oracle/,
@@ -59,6 +62,9 @@ def parse():
     ap.add_argument("--degree", type=int, default=None, help="override the workload degree")
     ap.add_argument("--n", type=int, default=None, help="override the workload size")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--strong", action="store_true",
+                    help="N>1: split ONE workload mesh into N cost-balanced row ranges (strong scaling, "
+                         "the paper's experiment) instead of one workload per rank (weak scaling, default)")
     ap.add_argument("--approach", type=int, default=2, choices=(1, 2),
                     help="2 = preset sparsity (default); 1 = stage-and-sort (triplets + device sort)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -252,7 +258,7 @@ def run_reference(args, w, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": w.description, "name": w.name, "degree": w.degree,
                                         "sample_elements": ref.pm.n_elements},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.cores, "kind": "port",
@@ -308,7 +314,7 @@ def run_ours(args, w, rank, world, local_rank):
         classify_boundary_faces(pm, coeffs)
         specs = build_basis(pm, w.degree)
     rows = None
-    if world > 1:
+    if world > 1 and args.strong:
         part = contiguous_partition(pm, world, quadrature_cost_weights(pm, specs))
         rows = part.owned[rank]
     stream = torch.cuda.Stream(dev)
@@ -410,7 +416,11 @@ def run_ours(args, w, rank, world, local_rank):
     el_ms_max = allmax(ms_el)
     h2d_tot, d2h_tot = allsum(h2d), allsum(d2h)
     launches_tot = allsum(launches / K)
-    n_el = pm.n_elements
+    # weak scaling (default for N>1): every rank assembles its own instance of the
+    # workload (independent meshes, no collective on the assembly path), so the
+    # units processed are N x the workload; strong: the ranks share one mesh
+    weak = world > 1 and not args.strong
+    n_el = pm.n_elements * (world if weak else 1)
     if rank != 0:
         return
     peak, peak_src = fp64_peak()
@@ -421,12 +431,15 @@ def run_ours(args, w, rank, world, local_rank):
         "metric": METRIC if not slab_case else "fp64 space-time slab assembly elements/s",
         "value": n_el / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if (world > 1 and args.strong) else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated mesh; analytic coefficients)",
         "config": {"workload": w.description, "name": w.name, "elements": n_el, "degree": w.degree,
                    "family": "P" if slab_case else None,
                    "dofs": int(plan.dof.n_dofs), "nnz": int(plan.nnz) if world == 1 else None,
-                   "parallelism": f"row-partitioned x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"row-partitioned x{world} (one mesh)" if args.strong else
+                                   f"x{world} ranks, one workload instance each (no collective)")
+                   if world > 1 else "single GPU",
+                   "elements_per_rank": pm.n_elements if weak else None,
                    "l2": "inputs+outputs >> 126 MB L2 (CSR written fresh each step), no flush needed"
                    if plan.nnz * 16 > 4e8 else "small workload: L2-resident",
                    "mesh_build_s": round(mesh_s, 1)},
