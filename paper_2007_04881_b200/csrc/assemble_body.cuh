@@ -433,8 +433,18 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           }
           if (cf.has_src()) {
             const double wf = w * cf.f(x);
+            // phi_f = X_a Y_b (Z_c): fold w f into the x-factors once (P+1 products
+            // instead of one per function)
+            constexpr MultiIdx<DIM, P> mi{};
+            double wx[P + 1];
 #pragma unroll
-            for (int f = 0; f < NB; ++f) rhs_add(f, wf * tb.val(f));
+            for (int k = 0; k <= P; ++k) wx[k] = wf * tb.v1[0][k];
+#pragma unroll
+            for (int f = 0; f < NB; ++f) {
+              double v = wx[mi.a[f][0]] * tb.v1[1][mi.a[f][1]];
+              if (DIM == 3) v *= tb.v1[2][mi.a[f][2]];
+              rhs_add(f, v);
+            }
           }
         }
         __syncwarp();
