@@ -554,15 +554,43 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       double* col = buf + slot;
       const int rv = mine ? 0 : 2;
       const double vs = mine ? 1.0 : -1.0;
+      if (DIM == 2 && !full) {
+        // phi = X_a Y_b: the trace sign, a(x) and the normal folded into the 1D
+        // factors once per point: V = X_a (s Y_b), F = (a n0 X'_a) Y_b + (a X_a)(n1 Y'_b)
+        constexpr MultiIdx<DIM, P> mi{};
+        double ys[P + 1], xa[P + 1], xb[P + 1], yc[P + 1];
 #pragma unroll
-      for (int ff = 0; ff < NBP; ++ff) {
-        double vv = 0.0, fl = 0.0;
-        if (ff < NB) {
-          vv = tb.val(ff);
-          if (grad_terms) fl = face_flux<DIM, P>(cf, tb, ff, nrm, av, A);
+        for (int k = 0; k <= P; ++k) {
+          ys[k] = vs * tb.v1[1][k];
+          xa[k] = (av * nrm[0]) * tb.d1[0][k];
+          xb[k] = av * tb.v1[0][k];
+          yc[k] = nrm[1] * tb.d1[1][k];
         }
-        col[(rv * NBP + ff) * KFP] = vs * vv;
-        col[((rv + 1) * NBP + ff) * KFP] = fl;
+#pragma unroll
+        for (int ff = 0; ff < NBP; ++ff) {
+          double vv = 0.0, fl = 0.0;
+          if (ff < NB) {
+            const int ia = mi.a[ff][0], ib = mi.a[ff][1];
+            vv = tb.v1[0][ia] * ys[ib];
+            if (grad_terms) {
+              if (ia > 0) fl = xa[ia] * tb.v1[1][ib];
+              if (ib > 0) fl = ia > 0 ? fma(xb[ia], yc[ib], fl) : xb[ia] * yc[ib];
+            }
+          }
+          col[(rv * NBP + ff) * KFP] = vv;
+          col[((rv + 1) * NBP + ff) * KFP] = fl;
+        }
+      } else {
+#pragma unroll
+        for (int ff = 0; ff < NBP; ++ff) {
+          double vv = 0.0, fl = 0.0;
+          if (ff < NB) {
+            vv = tb.val(ff);
+            if (grad_terms) fl = face_flux<DIM, P>(cf, tb, ff, nrm, av, A);
+          }
+          col[(rv * NBP + ff) * KFP] = vs * vv;
+          col[((rv + 1) * NBP + ff) * KFP] = fl;
+        }
       }
       if (mine) {
         double wbn = 0.0;
