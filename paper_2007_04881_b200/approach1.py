@@ -41,7 +41,7 @@ class Approach1Plan:
 
     def __init__(self, mesh, coeffs, specs, config: Optional[AssemblyConfig] = None, device=None, stream=None):
         torch = _torch()
-        self.base = SipgPlan(mesh, coeffs, specs, config, device=device, stream=stream)
+        self.base = SipgPlan(mesh, coeffs, specs, config, device=device, stream=stream, allocate_csr=False)
         b = self.base
         if b.jit_source is None:
             raise NotImplementedError("Approach 1 needs the runtime-specialised (NVRTC) kernels")
@@ -192,7 +192,12 @@ class Approach1Plan:
 
     @property
     def nnz(self) -> int:
-        return self.base.nnz  # the merged pattern equals the preset one (tests/test_approach1.py)
+        """Entries of the merged CSR (device count of the last merge; one sync
+        the first time it is read)."""
+        if not getattr(self, "_nnz", 0):
+            self.stream.synchronize()
+            self._nnz = int(self.t["nnz"].item())
+        return self._nnz
 
     @property
     def row_ptr(self):
@@ -200,11 +205,11 @@ class Approach1Plan:
 
     @property
     def col_idx(self):
-        return self.t["col_idx"][: self.base.nnz]
+        return self.t["col_idx"][: self.nnz]
 
     @property
     def values(self):
-        return self.t["values"][: self.base.nnz]
+        return self.t["values"][: self.nnz]
 
 
 def assemble_approach1_device(mesh, coeffs, specs, config: Optional[AssemblyConfig] = None):

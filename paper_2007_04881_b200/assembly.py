@@ -366,7 +366,8 @@ class SipgPlan:
     """
 
     def __init__(self, mesh, coeffs, specs, config: Optional[AssemblyConfig] = None,
-                 row_elements=None, device=None, stream=None, jit: bool = True):
+                 row_elements=None, device=None, stream=None, jit: bool = True,
+                 allocate_csr: bool = True):
         import ctypes as C
 
         torch = _torch()
@@ -477,9 +478,13 @@ class SipgPlan:
         pat.nbr_rec = _lib.ptr(self.t["nbr_rec"])
         self.pattern = pat
 
-        # size query (the one sync, like polydg's pattern build before values)
+        # size query (the one sync, like polydg's pattern build before values);
+        # allocate_csr=False (Approach 1 reuses the plan for mesh / rules / pre-pass
+        # only) skips both the sync and the 16 B/nnz CSR buffers
         with torch.cuda.stream(self.stream):
-            self._index_phase(size_query=True)
+            self._index_phase(size_query=allocate_csr)
+        if not allocate_csr:
+            self.nnz = 0
         self.t["col_idx"] = z(self.nnz, i64)
         self.t["values"] = z(self.nnz, torch.float64)
         self.t["rhs"] = torch.zeros(max(self.dof.n_dofs, 1), dtype=torch.float64, device=dev)

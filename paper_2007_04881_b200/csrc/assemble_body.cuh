@@ -68,11 +68,6 @@ namespace pdg {
     tprev = now_;                                \
   }
 
-// col_idx rows written with 16-byte stores (experiment, off: same-box A/B r01
-// cfg5 400k 8.04 vs 6.56 ms with 8-byte stores -- rejected)
-#ifndef PDG_COL_V2
-#define PDG_COL_V2 0
-#endif
 
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
@@ -666,37 +661,6 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       if (a.write_cols) {
         const int c0 = rc[0].col;
         const int c1 = rc[nw - 1].col + rc[nw - 1].nj;
-#if PDG_COL_V2
-        // 16-byte stores: lane m of an iteration owns columns c0+2m .. c0+2m+2;
-        // a row whose column c0 sits at an even address stores (2m, 2m+1), an
-        // odd one (2m+1, 2m+2) -- plus column c0 alone -- so every store is aligned
-        int q = 0;
-        auto cvat = [&](int p) -> long long {
-          while (q + 1 < nw && rc[q + 1].col <= p) ++q;
-          return (long long)(rc[q].dof + (p - rc[q].col));
-        };
-        const long long v00 = cvat(c0);
-        q = 0;
-        for (int pm = c0 + 2 * lane; pm < c1; pm += 64) {
-          const long long va = cvat(pm);
-          const long long vb = pm + 1 < c1 ? cvat(pm + 1) : 0;
-          const long long vc = pm + 2 < c1 ? cvat(pm + 2) : 0;
-          const bool pa = pm + 1 < c1, pb = pm + 2 < c1;
-#pragma unroll 4
-          for (int r = 0; r < ne; ++r) {
-            int64_t* row = pat.col_idx + voff + (int64_t)r * Lrow;
-            const bool odd = ((voff + (int64_t)r * Lrow + c0) & 1) != 0;
-            if (!odd) {
-              if (pa) *reinterpret_cast<longlong2*>(row + pm) = make_longlong2(va, vb);
-              else row[pm] = va;
-            } else {
-              if (pb) *reinterpret_cast<longlong2*>(row + pm + 1) = make_longlong2(vb, vc);
-              else if (pa) row[pm + 1] = vb;
-              if (pm == c0) row[c0] = v00;
-            }
-          }
-        }
-#else
         int q = 0;
         for (int p = c0 + lane; p < c1; p += 32) {
           while (q + 1 < nw && rc[q + 1].col <= p) ++q;
@@ -705,7 +669,6 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 #pragma unroll 4
           for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
         }
-#endif
       }
       PDG_T(4)
       int qi = 0;

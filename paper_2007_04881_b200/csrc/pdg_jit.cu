@@ -13,7 +13,8 @@
 // libnvrtc and libcuda are opened with dlopen on first use, so the library
 // itself links only against cudart (it must load on GPU-less build hosts).
 // Compiled cubins are cached in memory and on disk ($PDG_JIT_CACHE, default
-// <libdir>/jit_cache) keyed by the full source + options.
+// <libdir>/jit_cache) keyed by the full source + options + a content hash of
+// the included headers (PDG_SRC_HASH, set by the Makefile).
 #include <dlfcn.h>
 #include <unistd.h>
 
@@ -28,9 +29,12 @@
 #include <vector>
 
 #include "assemble_kernel.cuh"
-#include "assemble_ws.cuh"
 #include "slab_body.cuh"
 #include "approach1_body.cuh"
+
+#ifndef PDG_SRC_HASH
+#error "PDG_SRC_HASH must be defined by the build (content hash of the kernel headers)"
+#endif
 
 namespace pdg {
 
@@ -130,15 +134,6 @@ static int jit_rhs_regs_max() {
   return v ? atoi(v) : PDG_RHS_REGS_MAX;
 }
 
-// PDG_WS=1 selects the warp-specialised producer/consumer body
-// (assemble_ws.cuh) instead of the single-warp body (assemble_body.cuh).
-// Measured on 400k cfg5 cells (r1): single-warp 7.51 ms, WS 10.0 ms -- the
-// producer (tabulation + metadata) is the bottleneck, so WS is off by default.
-static bool jit_ws() {
-  const char* v = getenv("PDG_WS");
-  return v && v[0] == '1';
-}
-
 // PDG_JIT_WARPS: warps per CTA of the single-warp body (default 4).  Small CTAs
 // let the register budget, not the CTA granularity, set the resident warp count.
 // Default by dimension (measured r01, same box, cfg4 3D p=2: 4 warps x 3 CTAs
@@ -152,14 +147,12 @@ static int jit_warps(int dim) {
 
 static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv) {
   // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow.
-  // single-warp body: CTA = 128 threads, default 3 (168 registers, 12 warps/SM;
-  //   v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells);
-  // warp-specialised body: CTA = 64 threads (one pair), default 8 (128 registers)
-  const bool ws = jit_ws();
+  // CTA = 128 threads, default 3 (168 registers, 12 warps/SM;
+  //   v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells)
   const char* mb = getenv("PDG_JIT_MINBLOCKS");
-  const int minblocks = mb ? std::max(1, atoi(mb)) : (ws ? 8 : 12 / jit_warps(dim));
+  const int minblocks = mb ? std::max(1, atoi(mb)) : 12 / jit_warps(dim);
   std::ostringstream os;
-  os << "#include \"" << (ws ? "assemble_ws.cuh" : "assemble_body.cuh") << "\"\n"
+  os << "#include \"assemble_body.cuh\"\n"
      << "#include \"prepass_body.cuh\"\n"
      << "namespace pdg_jit {\nusing namespace pdg;\n"
      << policy << "\n}\n"
@@ -168,12 +161,10 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
   if (const char* mr = getenv("PDG_JIT_MAXNREG"))
     os << "__maxnreg__(" << atoi(mr) << ")";
   else
-    os << "__launch_bounds__(" << (ws ? 64 : 32 * jit_warps(dim)) << ", " << minblocks << ")";
+    os << "__launch_bounds__(" << 32 * jit_warps(dim) << ", " << minblocks << ")";
   os << " pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {\n"
-     << "  pdg::" << (ws ? "assemble_ws<" : "assemble_body<") << dim << ", " << P << ", "
-     << (sym ? "true" : "false");
-  if (!ws) os << ", pdg_jit::JitCoef, " << kv;
-  os << ">(a, pdg_jit::JitCoef());\n}\n";
+     << "  pdg::assemble_body<" << dim << ", " << P << ", " << (sym ? "true" : "false")
+     << ", pdg_jit::JitCoef, " << kv << ">(a, pdg_jit::JitCoef());\n}\n";
   // the face pre-pass with the same inlined fields (pdg_face_prepass_jit)
   os << "extern \"C\" __global__ void __launch_bounds__(256) pdg_jit_abar(const pdg_mesh m, const pdg_basis B, "
         "const pdg_rules R, const pdg_params prm, double* abar, uint32_t* flags) {\n"
@@ -209,7 +200,10 @@ static std::string get_module(const std::string& src, CUmod& out) {
     std::string tok;
     while (is >> tok) opts.push_back(tok);
   }
-  std::string key = src;
+  // the generated source only #includes the kernel headers, so their content
+  // hash (computed by the Makefile) and the ABI version are part of the key:
+  // a rebuilt library never loads a cubin compiled from older headers
+  std::string key = src + "\n// headers " PDG_SRC_HASH " abi " + std::to_string(PDG_ABI_VERSION);
   for (auto& o : opts) key += "\n" + o;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -326,7 +320,6 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     if (!pattern->nbr_rec) return fail(PDG_ERR_INVALID, "interface records missing (pdg_iface_records)");
     JitKernel k;
     const bool sym = symmetric_accumulation(*coeffs);
-    const bool ws = jit_ws();
     const bool has_vr = coeffs->has_advection || coeffs->has_reaction;
     KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values, write_col_idx,
                          rhs, err_flags, 0);
@@ -336,20 +329,13 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     int threads = 32 * jit_warps(mesh->dim);
     // the CTA's rule copy (always reserved: the JIT build may toggle PDG_RULES_SMEM)
     size_t smem = ((size_t)rule_smem_doubles(rules->n_points) + (size_t)a.lay.warp_doubles * (threads / 32)) * 8;
-    if (ws) {  // one producer/consumer pair per CTA: two stages + header + neighbour staging
-      int kv = 32;
-      a.lay.buf_doubles = ws_table_doubles(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, &kv);
-      a.lay.kv = kv;
-      threads = 64;
-      smem = (size_t)2 * (a.lay.buf_doubles + 64 + sizeof(WsHdr) / 8) * 8 + sizeof(NbrStage);
-    }
     Api& A = api();
     if (A.cuFuncSetAttribute(k.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES_, (int)smem) != 0)
       return fail(PDG_ERR_CUDA, "cuFuncSetAttribute(max dynamic smem) failed");
     int per_sm = 0;
     if (A.cuOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, threads, smem) != 0 || per_sm < 1) per_sm = 1;
-    const int64_t need = ws ? pattern->n_row_elements : (pattern->n_row_elements + threads / 32 - 1) / (threads / 32);
-    const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm * (ws ? 1 : 8));
+    const int64_t need = (pattern->n_row_elements + threads / 32 - 1) / (threads / 32);
+    const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm * 8);
     if (grid <= 0) return PDG_OK;
     void* args[] = {&a};
     if (A.cuLaunchKernel(k.fn, (unsigned)grid, 1, 1, threads, 1, 1, (unsigned)smem, (cudaStream_t)stream, args,

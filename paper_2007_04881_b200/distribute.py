@@ -97,7 +97,12 @@ def contiguous_partition(mesh, n_parts: int, weights: Optional[np.ndarray] = Non
     targets = cum[-1] * np.arange(1, n_parts) / n_parts
     cuts = np.searchsorted(cum, targets, side="left") + 1
     cuts = np.clip(cuts, np.arange(1, n_parts), nel - np.arange(n_parts - 1, 0, -1))
-    cuts = np.maximum.accumulate(cuts)
+    # strictly increasing, every part non-empty: forward pass cuts[k] >= cuts[k-1] + 1,
+    # backward pass cuts[k] <= nel - (n_parts - 1 - k)
+    for k in range(1, cuts.size):
+        cuts[k] = max(cuts[k], cuts[k - 1] + 1)
+    for k in range(cuts.size - 1, -1, -1):
+        cuts[k] = min(cuts[k], nel - (n_parts - 1 - k), cuts[k + 1] - 1 if k + 1 < cuts.size else nel)
     part_of = np.zeros(nel, dtype=np.int64)
     for c in cuts:
         part_of[c:] += 1

@@ -437,14 +437,29 @@ class PolytopicMesh:
 
 def flat_of(mesh) -> FlatMesh:
     """FlatMesh of this package's PolytopicMesh (no copy) or of any
-    polydg-style mesh object (adapter, cached on the object)."""
+    polydg-style mesh object (adapter, cached on the object).
+
+    The adapter is built once per polydg mesh and kept in ``mesh._pdg_flat``
+    (so its HBM copy, ``_device_cache``, is reused too).  Face tags are the
+    only field polydg mutates after construction (``classify_boundary_faces``,
+    model.py:164-173): they are re-read on every call and written into the
+    cached adapter in place, which ``DeviceMesh.refresh_tags`` then uploads."""
     if isinstance(mesh, FlatMesh):
         return mesh
     flat = getattr(mesh, "flat", None)
     if isinstance(flat, FlatMesh):
         return flat
+    flat = getattr(mesh, "_pdg_flat", None)
+    if isinstance(flat, FlatMesh) and flat.n_faces == len(mesh.faces):
+        tags = np.fromiter((tag_code(f.tag) for f in mesh.faces), np.int8, len(mesh.faces))
+        if not np.array_equal(tags, flat.face_tag):
+            flat.face_tag[:] = tags
+        return flat
     flat = FlatMesh.from_polytopic(mesh)
-    # tags may change between calls (classify_boundary_faces mutates them)
+    try:
+        object.__setattr__(mesh, "_pdg_flat", flat)
+    except Exception:  # slotted / frozen objects: no cache
+        pass
     return flat
 
 

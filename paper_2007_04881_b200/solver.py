@@ -66,38 +66,95 @@ class DeviceSystem:
         return y
 
 
-class BlockJacobiPreconditioner:
-    """Action of the inverse element-block diagonal (polydg solver.py:47-70)."""
+def _host_diagonal_blocks(matrix, offsets) -> list:
+    """Dense diagonal blocks of any host CSR (polydg ``_extract_diagonal_blocks``,
+    solver.py:30-44): entries outside the stored pattern are zero."""
+    rp, ci, va = np.asarray(matrix.row_ptr), np.asarray(matrix.col_idx), np.asarray(matrix.values)
+    rows = np.repeat(np.arange(rp.size - 1, dtype=np.int64), np.diff(rp))
+    elem = np.searchsorted(offsets, rows, "right") - 1
+    keep = (ci >= offsets[elem]) & (ci < offsets[elem + 1])
+    blocks = [np.zeros((int(offsets[e + 1] - offsets[e]),) * 2) for e in range(offsets.size - 1)]
+    for r, c, v, e in zip(rows[keep].tolist(), ci[keep].tolist(), va[keep].tolist(), elem[keep].tolist()):
+        blocks[e][r - offsets[e], c - offsets[e]] = v
+    return blocks
 
-    def __init__(self, system: DeviceSystem):
+
+class BlockJacobiPreconditioner:
+    """Action of the inverse element-block diagonal (polydg solver.py:47-70).
+
+    Block-structured CSRs (the assembled pattern) are inverted on the device.
+    Otherwise (``host`` = the host CSR) the dense diagonal blocks are extracted
+    on the host, as polydg does for any CSR.  Point Jacobi (1x1 blocks)
+    substitutes 1.0 for a zero or missing diagonal entry (polydg solver.py:102-104)."""
+
+    def __init__(self, system: DeviceSystem, offsets=None, host=None):
         import torch
 
         self.sys = system
-        counts = np.diff(system.dof.cpu().numpy())
+        offs = np.asarray(offsets if offsets is not None else system.dof.cpu().numpy(), np.int64)
+        self.dof = torch.from_numpy(offs).to(system.device)
+        self.n_blocks = int(offs.size - 1)
+        counts = np.diff(offs)
         off = np.concatenate([[0], np.cumsum(counts * counts)]).astype(np.int64)
         self.inv_off = torch.from_numpy(off).to(system.device)
-        self.inv = torch.empty(max(int(off[-1]), 1), dtype=torch.float64, device=system.device)
-        mx = int(counts.max()) if counts.size else 1
-        _lib.check(system.lib.pdg_block_jacobi_setup(
-            _lib.ptr(system.dof), system.n_elements, mx, _lib.ptr(system.row_ptr), _lib.ptr(system.col_idx),
-            _lib.ptr(system.values), _lib.ptr(self.inv_off), _lib.ptr(self.inv), _lib.ptr(system.flags),
-            _lib.stream_ptr(system.stream)))
-        system.stream.synchronize()
-        fl = int(system.flags.item())
-        if fl & 4:
-            raise SolverError("singular diagonal block")
-        if fl & 2:
-            raise SolverError("matrix has no diagonal block for some element")
+        point = bool(counts.size == 0 or counts.max() == 1)
+        if host is None:
+            self.inv = torch.empty(max(int(off[-1]), 1), dtype=torch.float64, device=system.device)
+            mx = int(counts.max()) if counts.size else 1
+            system.flags.zero_()
+            _lib.check(system.lib.pdg_block_jacobi_setup(
+                _lib.ptr(self.dof), self.n_blocks, mx, _lib.ptr(system.row_ptr), _lib.ptr(system.col_idx),
+                _lib.ptr(system.values), _lib.ptr(self.inv_off), _lib.ptr(self.inv), _lib.ptr(system.flags),
+                _lib.stream_ptr(system.stream)))
+            system.stream.synchronize()
+            fl = int(system.flags.item())
+            system.flags.zero_()
+            if fl and point:  # zero / missing diagonal entries: 1/d with d -> 1.0
+                d = _device_diagonal(system)
+                self.inv = torch.where(d != 0, 1.0 / torch.where(d != 0, d, 1.0), 1.0)
+                return
+            if fl & 4:
+                raise SolverError("singular diagonal block")
+            if fl & 2:
+                raise SolverError("matrix has no diagonal block for some element")
+            return
+        blocks = _host_diagonal_blocks(host, offs)
+        if point:
+            dg = np.array([b[0, 0] for b in blocks])
+            inv = [np.array([[1.0 / v if v != 0 else 1.0]]) for v in dg]
+        else:
+            inv = []
+            for b in blocks:
+                try:
+                    inv.append(np.linalg.inv(b))
+                except np.linalg.LinAlgError as exc:
+                    raise SolverError(f"singular diagonal block (size {b.shape[0]}): {exc}")
+        flat = np.concatenate([i.ravel() for i in inv]) if inv else np.zeros(1)
+        self.inv = torch.from_numpy(np.ascontiguousarray(flat)).to(system.device)
 
     def apply(self, r, out=None):
         import torch
 
         z = out if out is not None else torch.empty_like(r)
         s = self.sys
-        _lib.check(s.lib.pdg_block_jacobi_apply(_lib.ptr(s.dof), s.n_elements, _lib.ptr(self.inv_off),
+        _lib.check(s.lib.pdg_block_jacobi_apply(_lib.ptr(self.dof), self.n_blocks, _lib.ptr(self.inv_off),
                                                 _lib.ptr(self.inv), _lib.ptr(r), _lib.ptr(z),
                                                 _lib.stream_ptr(s.stream)))
         return z
+
+
+def _device_diagonal(system):
+    """Diagonal of the device CSR (0 where no entry is stored)."""
+    import torch
+
+    rp = system.row_ptr
+    n = system.n
+    lens = rp[1:] - rp[:-1]
+    rows = torch.repeat_interleave(torch.arange(n, device=system.device), lens)
+    hit = system.col_idx == rows
+    d = torch.zeros(n, dtype=torch.float64, device=system.device)
+    d.index_put_((rows[hit],), system.values[hit], accumulate=True)
+    return d
 
 
 def gmres_device(system: DeviceSystem, b, precond=None, tol=1e-10, restart=150, max_iter=2000):
@@ -188,21 +245,25 @@ def solve(matrix, rhs, tol: float = 1e-10, max_iter: int = 2000, restart: int = 
     if plan is not None:
         csr = _PlanCSR(plan)
         offsets = np.asarray(dof_map.offsets if dof_map is not None else plan.dof.offsets, np.int64)
+        pre_offsets, host = offsets, None
     else:
         csr = matrix
         if matrix.n_rows != matrix.n_cols:
             raise SolverError("solve needs a square matrix")
         offsets = (np.asarray(dof_map.offsets, np.int64) if dof_map is not None
                    else np.arange(matrix.n_rows + 1, dtype=np.int64))
+        pre_offsets, host = offsets, None
         if dof_map is not None and not _block_structured(matrix, offsets):
-            # a CSR without the assembled block structure: row blocks, point Jacobi
+            # a CSR without the assembled block structure: the SpMV runs on row
+            # blocks, the preconditioner keeps the element blocks (host extraction)
             offsets = np.arange(matrix.n_rows + 1, dtype=np.int64)
+            host = matrix
     sys_ = DeviceSystem(csr, offsets, device)
     b = torch.as_tensor(np.asarray(rhs, dtype=np.float64)).to(sys_.device)
     bnorm = float(torch.linalg.vector_norm(b))
     if bnorm == 0.0:
         return SolveResult(np.zeros(sys_.n), 0.0, 0, True)
-    pre = BlockJacobiPreconditioner(sys_)
+    pre = BlockJacobiPreconditioner(sys_, pre_offsets, host)
     x, iters = gmres_device(sys_, b, pre, tol, restart, max_iter)
     res = float(torch.linalg.vector_norm(b - sys_.matvec(x))) / bnorm
     sys_.stream.synchronize()

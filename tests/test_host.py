@@ -196,6 +196,17 @@ def test_contiguous_partition_balance_and_cut():
         partition_from_map(pm, np.r_[np.zeros(399, np.int64), [2]])  # part 1 empty
 
 
+def test_contiguous_partition_skewed_weights_keep_every_part_nonempty():
+    """One dominant weight used to collapse consecutive cuts onto the same index."""
+    pm = voronoi_mesh(400, seed=1)
+    w = np.ones(pm.n_elements)
+    w[1] = 1e6
+    for n in (2, 3, 4, 8):
+        part = contiguous_partition(pm, n, w)
+        assert all(o.size >= 1 for o in part.owned)
+        assert np.all(np.diff(part.part_of) >= 0)
+
+
 def test_quadrature_cost_weights_match_reference(polydg):
     from polydg import basis as RB, distribute as RD, mesh as RM
 

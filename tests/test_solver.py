@@ -81,3 +81,42 @@ def test_block_inverses_against_numpy():
         a, b = off[e], off[e + 1]
         ze = np.linalg.solve(A[a:b, a:b], r[a:b])
         assert np.allclose(z[a:b], ze, rtol=1e-10, atol=1e-12 * np.abs(ze).max())
+
+
+@pytest.mark.gpu
+def test_point_jacobi_zero_diagonal_substitutes_one():
+    """polydg solver.py:102-104: a zero or missing diagonal entry acts as 1.0."""
+    from paper_2007_04881_b200.solver import solve
+
+    # [[0, 1, 0], [1, 2, 0], [0, 0, 3]] with row 0's diagonal missing from the pattern
+    rp = np.array([0, 1, 3, 4], np.int64)
+    ci = np.array([1, 0, 1, 2], np.int64)
+    va = np.array([1.0, 1.0, 2.0, 3.0])
+    m = CSRMatrix(3, 3, rp, ci, va)
+    b = np.array([1.0, 2.0, 3.0])
+    res = solve(m, b, tol=1e-12)
+    assert res.converged
+    assert np.allclose(res.x, np.linalg.solve(m.to_dense(), b), rtol=1e-10)
+
+
+@pytest.mark.gpu
+def test_block_jacobi_on_unstructured_csr_keeps_element_blocks():
+    """A CSR without the assembled block structure (a dropped entry) still gets
+    element-block Jacobi (polydg extracts the blocks from any CSR)."""
+    from paper_2007_04881_b200.solver import BlockJacobiPreconditioner, _host_diagonal_blocks, solve
+
+    m, rhs, _, pattern = _system("adr", 2)
+    sp = m.to_scipy().tolil()
+    r0 = int(pattern.dof_map.offsets[3])
+    far = [c for c in sp.rows[r0] if c >= int(pattern.dof_map.offsets[4]) or c < int(pattern.dof_map.offsets[3])]
+    sp[r0, far[-1]] = 0.0
+    sp = sp.tocsr()
+    sp.eliminate_zeros()
+    m2 = CSRMatrix(m.n_rows, m.n_cols, sp.indptr.astype(np.int64), sp.indices.astype(np.int64), sp.data)
+    blocks = _host_diagonal_blocks(m2, pattern.dof_map.offsets)
+    A = m2.to_dense()
+    off = pattern.dof_map.offsets
+    for e in (0, 3, len(off) - 2):
+        assert np.array_equal(blocks[e], A[off[e]:off[e + 1], off[e]:off[e + 1]])
+    res = solve(m2, rhs, tol=1e-10, dof_map=pattern.dof_map)
+    assert res.converged and res.residual <= 1e-9

@@ -10,16 +10,16 @@ from paper_2007_04881_b200.model import policy_source  # noqa: E402
 from paper_2007_04881_b200.problems import WORKLOADS, coefficients  # noqa: E402
 
 
-def main(cfg="cfg5", degree=None, sym=True, minblocks=3, ws="0"):
+def main(cfg="cfg5", degree=None, sym=True, minblocks=3):
     w = WORKLOADS[cfg]
     p = w.degree if degree is None else int(degree)
     pol = policy_source(coefficients(w.coeffs, w.dim), w.dim)
-    body = "assemble_ws" if str(ws) == "1" else "assemble_body"
-    threads = 64 if str(ws) == "1" else 32 * int(os.environ.get("PDG_JIT_WARPS", "4"))
+    body = "assemble_body"
+    threads = 32 * int(os.environ.get("PDG_JIT_WARPS", "4"))
     sym = str(sym) not in ("0", "False", "false")
     mr = os.environ.get("PDG_JIT_MAXNREG")
     bounds = f"__maxnreg__({mr})" if mr else f"__launch_bounds__({threads}, {minblocks})"
-    tail = ", pdg_jit::JitCoef, 32" if body == "assemble_body" else ""
+    tail = ", pdg_jit::JitCoef, 32"
     src = (f'#include "{body}.cuh"\n#include "prepass_body.cuh"\nnamespace pdg_jit {{\nusing namespace pdg;\n'
            + pol + '\n}\n'
            f'extern "C" __global__ void {bounds} pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {{\n'
