@@ -7,12 +7,16 @@ wall ms at 1/2/4/8 B200, next to the host-CPU reference path).
 One step = one full assembly of the workload's rows on each rank: index
 phase (adjacency, row offsets), face pre-pass (sigma, flow side) and the fused
 element kernel (values + col_idx + RHS), with the mesh resident in HBM.
-Multi-GPU (torchrun): assembly needs no communication, so by
-default every rank assembles its own instance of the workload (weak scaling:
-value = N x elements / max-over-ranks time); ``--strong`` instead splits ONE
-mesh into contiguous, cost-balanced row ranges (the paper's strong-scaling
-experiment, one-sided cut faces).  No collective on the assembly path either
-way; timing is the max over ranks of CUDA-event time.
+Multi-GPU (torchrun): the paper's experiment -- ONE workload mesh split into
+N contiguous, cost-balanced parts (strong scaling, value =
+the mesh's elements / max-over-ranks time).  Each rank assembles ITS
+sub-mesh only (owned elements + one-ring halo, global columns:
+distribute.local_problem), so index phase, pre-pass and kernel all shrink
+with N; assembly needs no communication.  After the timed
+region one verification gather (NCCL point-to-point to rank 0) collects
+every rank's rows and rank 0 compares them bit for bit with the whole-mesh
+rows ("verified" in the JSON line).  ``--weak``: every rank assembles its
+own instance of the workload instead (value = N x elements / max time).
 ``e2e`` re-runs the step through the public plan API with the mesh copied
 from pinned host memory and the assembled CSR + RHS copied back every step.
 ``--impl reference`` times the CPU restatement of polydg's path (oracle/,
@@ -63,8 +67,11 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override the workload size")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--strong", action="store_true",
-                    help="N>1: split ONE workload mesh into N cost-balanced row ranges (strong scaling, "
-                         "the paper's experiment) instead of one workload per rank (weak scaling, default)")
+                    help="N>1: split ONE workload mesh into N cost-balanced parts (the default; kept as a no-op flag)")
+    ap.add_argument("--weak", action="store_true",
+                    help="N>1: one independent workload instance per rank (weak scaling) instead of the "
+                         "partitioned mesh")
+    ap.add_argument("--no-verify", action="store_true", help="N>1: skip the verification gather")
     ap.add_argument("--approach", type=int, default=2, choices=(1, 2),
                     help="2 = preset sparsity (default); 1 = stage-and-sort (triplets + device sort)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -278,7 +285,8 @@ def run_ours(args, w, rank, world, local_rank):
 
     from paper_2007_04881_b200 import _lib, build_basis, classify_boundary_faces
     from paper_2007_04881_b200.assembly import AssemblyConfig, HostIO, SipgPlan
-    from paper_2007_04881_b200.distribute import contiguous_partition, quadrature_cost_weights
+    from paper_2007_04881_b200.distribute import (contiguous_partition, gather_verify_partition, local_problem,
+                                                  quadrature_cost_weights)
     from paper_2007_04881_b200.problems import cached_mesh, coefficients
     from paper_2007_04881_b200.roofline import assembly_work
 
@@ -313,10 +321,15 @@ def run_ours(args, w, rank, world, local_rank):
         coeffs = coefficients(w.coeffs, w.dim)
         classify_boundary_faces(pm, coeffs)
         specs = build_basis(pm, w.degree)
-    rows = None
-    if world > 1 and args.strong:
+    rows, lp, part = None, None, None
+    partitioned = world > 1 and not args.weak
+    t_part = time.perf_counter()
+    if partitioned:
         part = contiguous_partition(pm, world, quadrature_cost_weights(pm, specs))
         rows = part.owned[rank]
+        if not slab_case and args.approach == 2:
+            lp = local_problem(pm, part, rank, specs, cfg)  # the rank's sub-mesh (host preprocessing)
+    part_s = time.perf_counter() - t_part
     stream = torch.cuda.Stream(dev)
     if slab_case:
         plan = SlabPlan(slab, coeffs, specs, initial, cfg, row_elements=rows, device=dev, stream=stream)
@@ -328,6 +341,10 @@ def run_ours(args, w, rank, world, local_rank):
             raise NotImplementedError("Approach 1 bench runs on one GPU")
         plan = Approach1Plan(pm, coeffs, specs, cfg, device=dev, stream=stream)
         work = assembly_work(plan.base)
+    elif lp is not None:
+        plan = SipgPlan(lp.flat, coeffs, lp.specs, lp.config, row_elements=lp.owned_local, device=dev,
+                        stream=stream, col_dof=lp.col_dof)
+        work = assembly_work(plan)
     else:
         plan = SipgPlan(pm, coeffs, specs, cfg, row_elements=rows, device=dev, stream=stream)
         work = assembly_work(plan)
@@ -416,36 +433,50 @@ def run_ours(args, w, rank, world, local_rank):
     el_ms_max = allmax(ms_el)
     h2d_tot, d2h_tot = allsum(h2d), allsum(d2h)
     launches_tot = allsum(launches / K)
-    # weak scaling (default for N>1): every rank assembles its own instance of the
-    # workload (independent meshes, no collective on the assembly path), so the
-    # units processed are N x the workload; strong: the ranks share one mesh
-    weak = world > 1 and not args.strong
+    flops_tot, bytes_tot = allsum(work["flops"]), allsum(work["bytes"])
+    nnz_tot = allsum(float(plan.nnz))
+    local_el = float(lp.flat.n_elements) if lp is not None else float(pm.n_elements)
+    local_el_max = allmax(local_el)
+    # weak scaling (--weak): every rank assembles its own instance of the
+    # workload, so the units processed are N x the workload; default: the
+    # ranks share one mesh
+    weak = world > 1 and args.weak
     n_el = pm.n_elements * (world if weak else 1)
+    verify = None
+    if partitioned and lp is not None and not args.no_verify and not args.profile:
+        torch.cuda.synchronize(dev)
+        verify = gather_verify_partition(plan, lp, part, pm, coeffs, specs, cfg)
     if rank != 0:
         return
     peak, peak_src = fp64_peak()
     hbm, hbm_src = hbm_peak()
-    achieved = work["flops"] / (ms_el * 1e-3) / 1e12
-    gbs = work["bytes"] / (ms_el * 1e-3) / 1e9
+    # whole-job algorithmic work over the slowest rank's element-kernel time
+    achieved = flops_tot / (el_ms_max * 1e-3) / 1e12 / world
+    gbs = bytes_tot / (el_ms_max * 1e-3) / 1e9 / world
     line = {
         "metric": METRIC if not slab_case else "fp64 space-time slab assembly elements/s",
         "value": n_el / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "strong" if (world > 1 and args.strong) else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated mesh; analytic coefficients)",
         "config": {"workload": w.description, "name": w.name, "elements": n_el, "degree": w.degree,
                    "family": "P" if slab_case else None,
-                   "dofs": int(plan.dof.n_dofs), "nnz": int(plan.nnz) if world == 1 else None,
-                   "parallelism": (f"row-partitioned x{world} (one mesh)" if args.strong else
+                   "dofs": int(specs_dofs(specs, w.dim)) if not slab_case else int(plan.dof.n_dofs),
+                   "nnz": int(nnz_tot) if not weak else int(plan.nnz),
+                   "parallelism": (f"partitioned x{world}: one mesh, contiguous cost-balanced parts, "
+                                   f"per-rank sub-mesh (owned + halo)" if partitioned else
                                    f"x{world} ranks, one workload instance each (no collective)")
                    if world > 1 else "single GPU",
                    "elements_per_rank": pm.n_elements if weak else None,
+                   "max_local_elements": int(local_el_max) if partitioned else None,
+                   "partition_s": round(part_s, 2) if partitioned else None,
                    "l2": "inputs+outputs >> 126 MB L2 (CSR written fresh each step), no flush needed"
                    if plan.nnz * 16 > 4e8 else "small workload: L2-resident",
                    "mesh_build_s": round(mesh_s, 1)},
         "phases_ms": {"index": ms_index, "prepass": ms_pre, "element_kernel": ms_el},
         "approach": args.approach if not slab_case else 2,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "per": "GPU (whole-job canonical FLOPs / N / slowest rank's element-kernel time)",
                      "frac": achieved / peak, "traffic": ncu_traffic(w.name, n_el),
                      "kernel": "pdg_slab_kernel (fused prism volume+lateral+bottom, DMMA f64)" if slab_case
                      else ("pdg_a1_kernel (Approach 1 item emission, DMMA f64)" if args.approach == 1
@@ -467,6 +498,12 @@ def run_ours(args, w, rank, world, local_rank):
             line["paper_p100_s_per_million_dofs"] = {
                 k: v[w.degree - 1] for k, v in PAPER_P100_S_PER_MDOF.items()}
             line["paper_p100_source"] = "PAPER.md:671-677 (Approach 2, fp64, 1x Tesla P100, not this metric's hardware)"
+    if verify is not None:
+        line["verified"] = "bitwise" if verify["verified"] else "MISMATCH"
+        line["verify_gather"] = {"bytes": verify["bytes"], "seconds": round(verify["seconds"], 2),
+                                 "how": "every rank's rows -> rank 0 (point-to-point, chunked), compared with "
+                                        "torch.equal against the whole-mesh rows of the same part",
+                                 "mismatch": verify["mismatch"]}
     if e2e_max is not None:
         line["e2e"] = {"value": n_el / (e2e_max * 1e-3), "unit": UNIT, "ms_per_step": e2e_max,
                        "h2d_bytes_per_step": int(h2d_tot), "d2h_bytes_per_step": int(d2h_tot)}
@@ -475,6 +512,12 @@ def run_ours(args, w, rank, world, local_rank):
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": sample}
     print(json.dumps(line), flush=True)
+
+
+def specs_dofs(specs, dim) -> int:
+    from paper_2007_04881_b200.assembly import DofMap
+
+    return DofMap.from_specs(specs).n_dofs
 
 
 def main():

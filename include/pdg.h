@@ -41,7 +41,7 @@ typedef unsigned long size_t;
 extern "C" {
 #endif
 
-#define PDG_ABI_VERSION 2
+#define PDG_ABI_VERSION 3
 
 typedef struct CUstream_st* pdg_stream; /* == cudaStream_t */
 
@@ -197,6 +197,10 @@ typedef struct pdg_pattern {
   int64_t* row_ptr;            /* [n_local_rows+1] */
   int64_t* col_idx;            /* [nnz] */
   pdg_iface_rec* nbr_rec;      /* [nbr_ptr[n_elements]] from pdg_iface_records (entries of owned rows) */
+  const int64_t* col_dof;      /* [n_elements] first GLOBAL column of each element's block, or NULL =
+                                  dof_offset.  Set when the mesh is a rank's sub-mesh (owned elements
+                                  + one-ring halo, monotone relabelling): the rows then carry the
+                                  global columns of the whole mesh (distribute.py:200-232) */
 } pdg_pattern;
 
 /* Affine frames, produced once per assembly by pdg_frames_build and read by
@@ -456,6 +460,34 @@ int pdg_map_simplices(const pdg_mesh* mesh, const pdg_rules* rules, int32_t orde
 int pdg_tabulate(const pdg_mesh* mesh, const pdg_basis* basis, int32_t element,
                  const double* points, int64_t n, double* values, double* grads,
                  pdg_stream stream);
+
+/* One face item of the unit face kernels (pdg_face_blocks). */
+enum { PDG_UNIT_INTERIOR = 0, PDG_UNIT_DIRICHLET = 1, PDG_UNIT_INFLOW = 2, PDG_UNIT_NEUMANN = 3 };
+typedef struct pdg_face_item {
+  int32_t face;   /* mesh face id */
+  int32_t kind;   /* PDG_UNIT_* */
+  int32_t upwind; /* interior: downwind (inflow) side 0 = owner, 1 = neighbour, -1 none
+                     (assembly.py:455-462); Dirichlet: 1 = owner inflow (with_inflow) */
+  int32_t pad_;
+  double sigma;   /* penalty (interior / Dirichlet) */
+} pdg_face_item;
+
+/* Unit face kernels (assembly.py:1160-1234): per item the four dense blocks
+ * (oo, on, no, nn) [n][4][nb][nb] of an interior face, or block [0] + load
+ * [n][nb] of a Dirichlet / inflow / Neumann face, summed over the face's
+ * sub-facets; nb = num_basis(max_degree), unused entries zero.  Rules must
+ * hold the face orders 2*max(p_o, p_n) + quad_increment.  Coefficients are
+ * interpreted (bytecode, numpy-identical trigonometry). */
+int pdg_face_blocks(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
+                    const pdg_rules* rules, const pdg_params* params, const pdg_face_item* items,
+                    int64_t n, double* blocks, double* loads, uint32_t* err_flags, pdg_stream stream);
+
+/* Every coefficient field at n points [n][dim] -> out [n][dim*dim + dim + 4]:
+ * A (row-major; an isotropic a(x) on the diagonal), b, c, f, g_D, g_N; absent
+ * fields are 0 (model.py:38-55; the a_bar input of penalty_side_data,
+ * model.py:196-235). */
+int pdg_eval_coeffs(int32_t dim, const pdg_coeffs* coeffs, const double* points, int64_t n, double* out,
+                    pdg_stream stream);
 
 /* Dense per-element volume blocks [n][nb][nb] and loads [n][nb]
  * (assembly.py:1139-1152); nb = num_basis(max_degree). */

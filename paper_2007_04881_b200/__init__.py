@@ -20,6 +20,7 @@ from .model import (
     ClassificationError,
     PdeCoefficients,
     PenaltyConfig,
+    PenaltySideData,
     ScalarField,
     TensorField,
     VectorField,
@@ -28,6 +29,8 @@ from .model import (
     constant_tensor,
     constant_vector,
     isotropic_diffusion,
+    penalty_side_data,
+    penalty_sigma,
     scalar_diffusion,
 )
 from .quadrature import QuadratureError
@@ -45,8 +48,14 @@ from .assembly import (
     assemble_approach2,
     assemble_device,
     build_block_pattern,
+    dirichlet_kernel,
     element_kernel,
+    inflow_kernel,
+    interior_face_kernel,
+    neumann_outflow_kernel,
+    triplets_to_csr,
 )
+from .kernels import eval_coefficients, face_sigma, map_simplices, tabulate
 from .distribute import (
     PartialMatrix,
     Partition,

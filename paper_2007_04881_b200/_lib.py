@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpdg.so")
 
 PDG_OK, PDG_ERR_INVALID, PDG_ERR_CUDA, PDG_ERR_UNSUPPORTED = 0, 1, 2, 3
-ABI_VERSION = 2  # include/pdg.h PDG_ABI_VERSION
+ABI_VERSION = 3  # include/pdg.h PDG_ABI_VERSION
 FLAG_DEGENERATE_SIMPLEX = 1 << 0
 FLAG_DEGENERATE_FACET = 1 << 1
 FLAG_STRADDLE = 1 << 2
@@ -83,7 +83,7 @@ class Pattern(C.Structure):
     _fields_ = [("n_row_elements", _i64), ("row_elements", _p),
                 ("nbr_ptr", _p), ("nbr_elem", _p), ("nbr_iface", _p),
                 ("row_len", _p), ("elem_val_offset", _p), ("elem_row_offset", _p),
-                ("row_ptr", _p), ("col_idx", _p), ("nbr_rec", _p)]
+                ("row_ptr", _p), ("col_idx", _p), ("nbr_rec", _p), ("col_dof", _p)]
 
 
 class Frames(C.Structure):
@@ -110,6 +110,12 @@ class AggOut(C.Structure):
                [("n_faces", _i64), ("n_facets", _i64), ("n_interfaces", _i64), ("n_interior_faces", _i64)]
 
 
+class FaceItem(C.Structure):
+    _fields_ = [("face", _i32), ("kind", _i32), ("upwind", _i32), ("pad_", _i32), ("sigma", C.c_double)]
+
+
+UNIT_INTERIOR, UNIT_DIRICHLET, UNIT_INFLOW, UNIT_NEUMANN = 0, 1, 2, 3  # include/pdg.h PDG_UNIT_*
+
 SLAB_MAX_DEGREE = {"P": 5, "PQ": 4}  # include/pdg.h PDG_SLAB_MAX_DEGREE(_PQ)
 
 #: every symbol include/pdg.h declares (checked by the CPU test suite)
@@ -120,7 +126,7 @@ EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspa
            "pdg_a1_emit", "pdg_triplets_workspace_bytes", "pdg_triplets_to_csr", "pdg_triplets_to_vector",
            "pdg_agglomerate_workspace_bytes", "pdg_agglomerate",
            "pdg_spmv_blocked", "pdg_block_jacobi_setup", "pdg_block_jacobi_apply",
-           "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks")
+           "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks", "pdg_face_blocks", "pdg_eval_coeffs")
 
 
 class EngineUnavailable(RuntimeError):
@@ -177,6 +183,9 @@ def load():
     lib.pdg_tabulate.argtypes = [P(Mesh), P(Basis), _i32, _p, _i64, _p, _p, _p]
     lib.pdg_element_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params),
                                        P(Frames), _p, _i64, _p, _p, _p, _p]
+    lib.pdg_face_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params), _p, _i64, _p, _p,
+                                    _p, _p]
+    lib.pdg_eval_coeffs.argtypes = [_i32, P(Coeffs), _p, _i64, _p, _p]
     for name in EXPORTS:
         if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes",
                         "pdg_triplets_workspace_bytes", "pdg_agglomerate_workspace_bytes"):

@@ -219,6 +219,7 @@ class AssemblyStats:
     triplet_count: int = 0
     nnz: int = 0
     device_ms: dict = field(default_factory=dict)
+    kernel_split: str = ""
 
     @property
     def duplicate_ratio(self) -> float:
@@ -367,7 +368,7 @@ class SipgPlan:
 
     def __init__(self, mesh, coeffs, specs, config: Optional[AssemblyConfig] = None,
                  row_elements=None, device=None, stream=None, jit: bool = True,
-                 allocate_csr: bool = True):
+                 allocate_csr: bool = True, col_dof=None):
         import ctypes as C
 
         torch = _torch()
@@ -476,6 +477,13 @@ class SipgPlan:
             _lib.ptr(self.t["row_len"]), _lib.ptr(self.t["val_off"]), _lib.ptr(self.t["row_off"]))
         pat.row_ptr = _lib.ptr(self.t["row_ptr"])
         pat.nbr_rec = _lib.ptr(self.t["nbr_rec"])
+        self.col_dof = None
+        if col_dof is not None:  # a rank's sub-mesh: rows carry the whole mesh's columns
+            self.col_dof = np.ascontiguousarray(col_dof, np.int64)
+            if self.col_dof.shape != (nel,):
+                raise ValueError("col_dof needs one global DoF offset per element")
+            self.t["col_dof"] = T(self.col_dof)
+            pat.col_dof = _lib.ptr(self.t["col_dof"])
         self.pattern = pat
 
         # size query (the one sync, like polydg's pattern build before values);
@@ -744,6 +752,7 @@ class DeviceAssembly:
 
     plan: SipgPlan
     stats: AssemblyStats
+    local: object = None  # distribute.LocalProblem when the plan runs on a rank's sub-mesh
 
     @property
     def row_ptr(self):
@@ -766,27 +775,57 @@ class DeviceAssembly:
 
 
 def assemble_device(mesh, coeffs, specs, config: Optional[AssemblyConfig] = None,
-                    row_elements=None, device=None, stream=None) -> DeviceAssembly:
+                    row_elements=None, device=None, stream=None, col_dof=None) -> DeviceAssembly:
     """Assemble on the GPU and keep the CSR in HBM."""
     torch = _torch()
     t0 = time.perf_counter()
-    plan = SipgPlan(mesh, coeffs, specs, config, row_elements, device, stream)
+    plan = SipgPlan(mesh, coeffs, specs, config, row_elements, device, stream, col_dof=col_dof)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     plan.run(ev)
     plan.check_flags()
     ms_index = ev[0].elapsed_time(ev[1])
     ms_pre = ev[1].elapsed_time(ev[2])
     ms_el = ev[2].elapsed_time(ev[3])
-    kern = plan.work_stats()
-    kern["element"].seconds = ms_el * 1e-3      # fused volume + face + boundary kernel
-    kern["interior"].seconds = ms_pre * 1e-3    # sigma / flow-side pre-pass
-    stats = AssemblyStats(
-        kernels=kern, index_seconds=ms_index * 1e-3,
-        kernel_wall_seconds=(ms_pre + ms_el) * 1e-3,
-        total_seconds=time.perf_counter() - t0,
-        triplet_count=sum(k.nnz_written for k in kern.values()), nnz=plan.nnz,
-        device_ms={"index": ms_index, "prepass": ms_pre, "element": ms_el})
+    stats = _stats(plan, ms_index, ms_pre, ms_el, time.perf_counter() - t0)
     return DeviceAssembly(plan, stats)
+
+
+def apportion(kern: dict, flops: dict, ms: float) -> None:
+    """Split one fused kernel's device time ``ms`` across polydg's kernel rows
+    in proportion to their canonical FLOPs (the rows sum to ``ms``)."""
+    tot = sum(flops.values())
+    for name, fl in flops.items():
+        kern[name].seconds = ms * 1e-3 * (fl / tot if tot > 0 else (1.0 if name == "element" else 0.0))
+
+
+def _stats(plan, ms_index, ms_pre, ms_el, total_s) -> AssemblyStats:
+    """polydg ``AssemblyStats`` (assembly.py:360-391) of one device assembly.
+
+    Mapping of polydg's timers onto the device phases:
+      * ``index_seconds`` = the index phase (adjacency, row offsets), polydg's
+        ``_pattern_from_adjacency`` + ``empty_matrix``;
+      * ``kernel_wall_seconds`` = the fused element kernel, polydg's
+        ``_execute_plan`` wall;
+      * the pre-pass (frames, sigma, flow side, interface records) is polydg's
+        ``build_work_plan`` work, which polydg times in no kernel row: here too
+        it is only in ``total_seconds`` (and ``device_ms["prepass"]``);
+      * per-kernel ``seconds``: ONE kernel computes every class, so its device
+        time is split across the five rows in proportion to each class's
+        canonical FLOPs (roofline.assembly_work; the rows sum to the kernel
+        time) -- an apportioned figure, flagged by ``kernel_split``.
+    ``work_items`` / ``nnz_written`` are polydg's analytic counts."""
+    from .roofline import assembly_work
+
+    kern = plan.work_stats()
+    w = assembly_work(plan)
+    apportion(kern, {"element": w["flops_volume"], "interior": w["flops_interior"],
+                     "dirichlet": w["flops_dirichlet"], "inflow": w["flops_inflow"],
+                     "neumann_outflow": w["flops_neumann"]}, ms_el)
+    return AssemblyStats(
+        kernels=kern, index_seconds=ms_index * 1e-3, kernel_wall_seconds=ms_el * 1e-3, total_seconds=total_s,
+        triplet_count=sum(k.nnz_written for k in kern.values()), nnz=plan.nnz,
+        device_ms={"index": ms_index, "prepass": ms_pre, "element": ms_el},
+        kernel_split="apportioned by canonical FLOPs (one fused kernel)")
 
 
 # ---------------------------------------------------------------------------
@@ -832,6 +871,50 @@ def _assemble_approach2_rows(mesh, coeffs, specs, config, row_elements):
     _check_classified(mesh)
     res = assemble_device(mesh, coeffs, specs, config, row_elements=row_elements)
     return res
+
+
+def triplets_to_csr(rows, cols, vals, n_rows, n_cols, n_workers=1, sentinel=None) -> CSRMatrix:
+    """Sort triplets by (row, col), sum duplicates in stable input order, emit
+    CSR (polydg ``assembly.py:1002-1031``) -- on the device: 64-bit keys
+    row * n_cols + col, CUB stable radix sort + reduce-by-key
+    (``pdg_triplets_to_csr``).  ``n_workers`` is accepted for compatibility
+    (the result never depends on it, as in polydg)."""
+    import ctypes as C
+
+    torch = _torch()
+    rows = np.asarray(rows, dtype=np.int64).ravel()
+    cols = np.asarray(cols, dtype=np.int64).ravel()
+    vals = np.asarray(vals, dtype=float).ravel()
+    if not (rows.shape == cols.shape == vals.shape):
+        raise ValueError("rows, cols and vals must have the same length")
+    if sentinel is not None:
+        keep = rows != sentinel
+        rows, cols, vals = rows[keep], cols[keep], vals[keep]
+    if rows.size == 0:
+        return CSRMatrix(n_rows, n_cols, np.zeros(n_rows + 1, dtype=np.int64), np.empty(0, dtype=np.int64),
+                         np.empty(0))
+    if rows.min() < 0 or rows.max() >= n_rows or cols.min() < 0 or cols.max() >= n_cols:
+        raise AssemblyError("triplet index out of matrix bounds")
+    if int(n_rows) * int(n_cols) >= (1 << 63):
+        raise AssemblyError("matrix too large for 64-bit triplet keys")
+    dev = _require_cuda(None)
+    lib = _lib.load()
+    n = int(rows.size)
+    keys = torch.from_numpy(rows * np.int64(n_cols) + cols).to(dev)
+    tv = torch.from_numpy(np.ascontiguousarray(vals)).to(dev)
+    rp = torch.empty(int(n_rows) + 1, dtype=torch.int64, device=dev)
+    ci = torch.empty(n, dtype=torch.int64, device=dev)
+    va = torch.empty(n, dtype=torch.float64, device=dev)
+    nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+    wsb = int(lib.pdg_triplets_workspace_bytes(n))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    _lib.check(lib.pdg_triplets_to_csr(_lib.ptr(keys), _lib.ptr(tv), n, int(n_rows), int(n_cols), _lib.ptr(rp),
+                                       _lib.ptr(ci), _lib.ptr(va), _lib.ptr(nnz), _lib.ptr(ws), wsb,
+                                       _lib.stream_ptr(stream)))
+    stream.synchronize()
+    k = int(nnz.item())
+    return CSRMatrix(int(n_rows), int(n_cols), rp.cpu().numpy(), ci[:k].cpu().numpy(), va[:k].cpu().numpy())
 
 
 def build_block_pattern(mesh, specs, row_elements=None) -> BlockPattern:
@@ -917,3 +1000,11 @@ class _UnitPlan:
         fr.simplex, fr.facet, fr.element = (_lib.ptr(self.t["sframe"]), _lib.ptr(self.t["fframe"]),
                                             _lib.ptr(self.t["erec"]))
         self.frames = fr
+
+
+from .kernels import (  # noqa: E402  polydg assembly.py:1160-1234 live in kernels.py
+    dirichlet_kernel,
+    inflow_kernel,
+    interior_face_kernel,
+    neumann_outflow_kernel,
+)

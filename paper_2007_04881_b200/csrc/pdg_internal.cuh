@@ -61,8 +61,8 @@ __device__ __forceinline__ void write_col_rows(const pdg_basis& B, const pdg_pat
     int64_t cs = 0, q = q0, d0 = 0;
     for (; q < q1; ++q) {
       const int32_t j = P.nbr_elem[q];
-      d0 = B.dof_offset[j];
-      const int64_t nj = B.dof_offset[j + 1] - d0;
+      const int64_t nj = B.dof_offset[j + 1] - B.dof_offset[j];
+      d0 = P.col_dof ? P.col_dof[j] : B.dof_offset[j];
       if (p < cs + nj) break;
       cs += nj;
     }

@@ -523,6 +523,7 @@ extern "C" int pdg_slab_assemble(const pdg_mesh* mesh, const pdg_basis* basis, c
         !pattern->elem_val_offset)
       return fail(PDG_ERR_INVALID, "pattern not built (pdg_adjacency / pdg_pattern_offsets)");
     if (!pattern->nbr_rec) return fail(PDG_ERR_INVALID, "interface records missing (pdg_iface_records)");
+    if (pattern->col_dof) return fail(PDG_ERR_UNSUPPORTED, "slab assembly of a sub-mesh (col_dof) is not supported");
     if (pattern->n_row_elements <= 0) return PDG_OK;
     const int S = mesh->dim, P = basis->max_degree, fam = slab->family, nw = slab_warps(S, P, fam);
     CUmod mod = nullptr;

@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(128) iface_records_kernel(const pdg_mesh m, co
       long long dof = 0;
       if (gl < nv) {
         j = P.nbr_elem[q];
-        dof = B.dof_offset[j];
-        nj = (int)(B.dof_offset[j + 1] - dof);
+        nj = (int)(B.dof_offset[j + 1] - B.dof_offset[j]);
+        dof = P.col_dof ? P.col_dof[j] : B.dof_offset[j];
         pj = B.degree[j];
         if (j != e) {
           const int32_t ifc = P.nbr_iface[q];

@@ -384,6 +384,18 @@ class PolytopicMesh:
         self.agg_map = agg_map
         self.flat = flat
 
+    @classmethod
+    def from_flat(cls, flat: FlatMesh) -> "PolytopicMesh":
+        """Object view of a FlatMesh (no validation: the arrays already are
+        an agglomerated mesh, e.g. a cached workload mesh or a rank's sub-mesh)."""
+        base = SimplicialMesh.__new__(SimplicialMesh)
+        base.dim, base.vertices, base.simplex_volumes = flat.dim, flat.vertices, flat.simplex_volumes
+        base.simplices = flat.simplices.astype(np.int64)
+        agg = np.repeat(np.arange(flat.n_elements), np.diff(flat.elem_ptr))
+        agg_full = np.empty_like(agg)
+        agg_full[flat.elem_simplices] = agg
+        return cls(base, agg_full, flat)
+
     @property
     def dim(self) -> int:
         return self.flat.dim

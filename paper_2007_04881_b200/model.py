@@ -274,6 +274,70 @@ class PenaltyConfig:
         return bool(self.coverable is not None and self.coverable[element])
 
 
+@dataclass
+class PenaltySideData:
+    """Per-side penalty inputs (polydg ``model.py:77-87``)."""
+
+    volume: float
+    degree: int
+    a_bar: float
+    max_adjacent_volume: float
+    cov_cap: float
+
+
+def penalty_side_data(mesh, element: int, face, degree: int, volume_points, coeffs,
+                      config: PenaltyConfig) -> PenaltySideData:
+    """Per-side penalty inputs (polydg ``model.py:196-235``): ``a_bar`` =
+    max over ``volume_points`` of n.A(x)n with the face normal, evaluated by
+    the device coefficient kernel (``pdg_eval_coeffs``); the largest
+    subdivision simplex of ``element`` touching the face; the coverability
+    cap p^(2(d-1))."""
+    from .kernels import _face_id, eval_coefficients
+    from .mesh import BOUNDARY, MeshError, flat_of
+
+    flat = flat_of(mesh)
+    fid = _face_id(mesh, face)
+    n = np.asarray(flat.face_normal[fid], float)
+    if coeffs.diffusion is None:
+        a_bar = 0.0
+    else:
+        a = eval_coefficients(coeffs, np.asarray(volume_points, float))["diffusion"]
+        a_bar = float(np.einsum("i,qij,j->q", n, a, n).max())
+    rows = slice(int(flat.face_ptr[fid]), int(flat.face_ptr[fid + 1]))
+    if element == int(flat.face_owner[fid]):
+        adj = flat.facet_owner_simplex[rows]
+    elif element == int(flat.face_neighbor[fid]):
+        adj = flat.facet_neighbor_simplex[rows]
+    else:
+        raise MeshError("element is not adjacent to the face")
+    adj = adj[adj != BOUNDARY]
+    if adj.size == 0:
+        raise MeshError("no subdivision simplex adjacent to the face")
+    max_adj = float(flat.simplex_volumes[adj].max())
+    d = flat.dim
+    cov_cap = float(degree ** (2 * (d - 1))) if config.is_coverable(element) else np.inf
+    return PenaltySideData(volume=float(flat.elem_volumes[element]), degree=int(degree), a_bar=a_bar,
+                           max_adjacent_volume=max_adj, cov_cap=cov_cap)
+
+
+def penalty_sigma(face, owner_data: PenaltySideData, neighbor_data: Optional[PenaltySideData],
+                  config: PenaltyConfig) -> float:
+    """sigma = C max_k min(|k| / sup|K^F|, cov_cap) a_bar p^2 |F| / |k|, over the
+    owner only on Dirichlet faces (polydg ``model.py:238-257``).  The assembly
+    path computes the same value for every face on the device
+    (``kernels.face_sigma``, csrc/prepass_body.cuh)."""
+    from .mesh import MeshError
+
+    sides = [owner_data] if neighbor_data is None else [owner_data, neighbor_data]
+    best = 0.0
+    for s in sides:
+        if s.max_adjacent_volume <= 0.0:
+            raise MeshError("penalty data has no adjacent subdivision simplex")
+        ratio = min(s.volume / s.max_adjacent_volume, s.cov_cap)
+        best = max(best, ratio * s.a_bar * s.degree ** 2 * float(face.measure) / s.volume)
+    return config.constant * best
+
+
 # ---------------------------------------------------------------------------
 # conversion of arbitrary coefficient objects into device descriptors
 # ---------------------------------------------------------------------------
@@ -547,7 +611,15 @@ def _is_zero(e) -> bool:
 
 
 def _policy(coeffs, dim: int, initial=None, sinpi: bool = True):
+    # sinpi lowering only for the volume fields (A, c, f: a 1-ulp argument
+    # difference is invisible there).  Fields evaluated on faces -- the
+    # Dirichlet / Neumann data, the advection field that decides inflow /
+    # upwinding, the initial data -- keep the reference's sin(fl(k*pi)*u):
+    # on a boundary that is a zero of the field (polydg's manufactured
+    # solutions, model.py:312-358) sin(fl(pi)) = 1.2e-16, not 0, and the
+    # penalty amplifies the difference to ~1e-11 of the element's RHS.
     cuda_expr_ = lambda e: cuda_expr(e, sinpi)
+    exact_ = lambda e: cuda_expr(e, False)
     ten = as_tensor(coeffs.diffusion, dim, "diffusion")
     kind, ent = 0, None
     if ten is not None:
@@ -600,14 +672,15 @@ def _policy(coeffs, dim: int, initial=None, sinpi: bool = True):
                f"{{ switch (i * {dim} + j) {{ {cases} default: break; }} return 0.0; }}")
     cases = ""
     if adv is not None:
-        cases = " ".join(f"case {k}: return {cuda_expr_(e)};" for k, e in enumerate(adv))
+        cases = " ".join(f"case {k}: return {exact_(e)};" for k, e in enumerate(adv))
     out.append(f"  __device__ double b_i(int i, const double* x) const "
                f"{{ switch (i) {{ {cases} default: break; }} return 0.0; }}")
     for n in ("c", "f", "gD", "gN"):
-        body = cuda_expr_(sc[n]) if sc[n] is not None else "0.0"
+        lower = cuda_expr_ if n in ("c", "f") else exact_
+        body = lower(sc[n]) if sc[n] is not None else "0.0"
         out.append(f"  __device__ double {n}(const double* x) const {{ return {body}; }}")
     out.append(f"  __device__ double u0(const double* x) const "
-               f"{{ return {cuda_expr_(u0) if u0 is not None else '0.0'}; }}")
+               f"{{ return {exact_(u0) if u0 is not None else '0.0'}; }}")
     out.append("};")
     info = dict(kind=kind, diag=diag, n_active=sum(nz[i][i] for i in range(dim)),
                 adv=adv is not None, reac=sc["c"] is not None, src=sc["f"] is not None,

@@ -64,9 +64,10 @@ class Workload:
     degree: int
     coeffs: str
     seed: int
+    mesh: str = ""   # workloads sharing a mesh (the cfg3 degree sweep) name it here
 
     def key(self) -> str:
-        return f"{self.name}_d{self.dim}_n{self.n}_k{self.k}_s{self.seed}"
+        return f"{self.mesh or self.name}_d{self.dim}_n{self.n}_k{self.k}_s{self.seed}"
 
 
 WORKLOADS = {
@@ -81,6 +82,13 @@ WORKLOADS = {
     "cfg5": Workload("cfg5", "2D diffusion (Poisson), p=4, 4M-element Voronoi mesh", 2, 4_000_000, 0, 4,
                      "poisson_sine", 3),
 }
+
+# cfg3's p = 2..6 sweep (BASELINE.json configs[2]): one 250k-cell mesh, one
+# workload per degree ("cfg3" itself is the p = 4 point)
+for _p in (2, 3, 4, 5, 6):
+    WORKLOADS[f"cfg3p{_p}"] = Workload(
+        f"cfg3p{_p}", f"2D advection-diffusion-reaction, upwinded faces, p={_p}, 250k Voronoi", 2, 250_000, 0,
+        _p, "adr", 2, mesh="cfg3")
 
 # Space-time slab workloads (the paper's single-GPU tables,
 # one slab of a linear parabolic problem, family P =
@@ -119,14 +127,7 @@ def cached_mesh(w: Workload, cache_dir: str = "/tmp/pdg_meshcache") -> Polytopic
         with open(meta) as fh:
             info = json.load(fh)
         arrs = {k: np.load(os.path.join(d, k + ".npy")) for k in info["fields"]}
-        flat = FlatMesh(dim=info["dim"], **arrs)
-        base = SimplicialMesh.__new__(SimplicialMesh)
-        base.dim, base.vertices, base.simplex_volumes = flat.dim, flat.vertices, flat.simplex_volumes
-        base.simplices = flat.simplices.astype(np.int64)
-        agg = np.repeat(np.arange(flat.n_elements), np.diff(flat.elem_ptr))
-        agg_full = np.empty_like(agg)
-        agg_full[flat.elem_simplices] = agg
-        return PolytopicMesh(base, agg_full, flat)
+        return PolytopicMesh.from_flat(FlatMesh(dim=info["dim"], **arrs))
     pm = build_mesh(w)
     try:
         tmp = d + f".tmp{os.getpid()}"

@@ -64,6 +64,8 @@ def assembly_work(plan) -> dict:
     inflow = (~inter) & (tag == TAG_CODE["inflow"]) & owned[o]
     face_d = float(np.sum((4.0 * n[o] ** 2 * nqf * nfac)[dirich]))  # inflow part not known host-side
     face_i = float(np.sum((2.0 * n[o] ** 2 * nqf * nfac)[inflow]))
+    neu = (~inter) & (tag == TAG_CODE["neumann"]) & owned[o]
+    face_n = float(np.sum((2.0 * n[o] * nqf * nfac)[neu]))  # load only
     flops = vol + face_int + face_d + face_i
 
     nnz = float(plan.nnz)
@@ -71,7 +73,8 @@ def assembly_work(plan) -> dict:
     geo = float(np.sum(nsim[owned])) * 8.0 * d * (d + 1) + float(np.sum(nfac[inter | owned[o]])) * (8.0 * d * d + 32)
     bytes_ = 16.0 * nnz + 8.0 * nrows * 2 + geo
     return {"flops": flops, "bytes": bytes_, "flops_volume": vol, "flops_faces": face_int + face_d + face_i,
-            "nnz": nnz, "elements": float(owned.sum())}
+            "flops_interior": face_int, "flops_dirichlet": face_d, "flops_inflow": face_i,
+            "flops_neumann": face_n, "nnz": nnz, "elements": float(owned.sum())}
 
 
 def slab_work(plan) -> dict:
@@ -112,4 +115,5 @@ def slab_work(plan) -> dict:
     geo = float(np.sum(nsim[owned])) * 8.0 * 6 + float(np.sum(nfac[inter | owned[o]])) * 40.0
     bytes_ = 16.0 * nnz + 16.0 * float(plan.n_local_rows) + geo
     return {"flops": flops, "bytes": bytes_, "flops_volume": vol, "flops_faces": face_int + face_d + bottom,
+            "flops_interior": face_int, "flops_dirichlet": face_d, "flops_bottom": bottom,
             "nnz": nnz, "elements": float(owned.sum()), "family": family_name(plan.family)}

@@ -167,6 +167,34 @@ def adr(dim):
                              dirichlet_data=M.constant_scalar(0.0))
 
 
+def advdiff3d(dim=3):
+    """polydg ``advection_diffusion_3d_problem`` (model.py:312-358): A = 0.01 I,
+    b = 1 + x, c = 3 + xyz, u = sin(pi x) sin(pi y) sin(pi z) as Dirichlet data
+    (zero on the cube's faces only up to sin(fl(pi)) = 1.2e-16), f manufactured."""
+    pi = np.pi
+    sx, sy, sz = M.sin(pi * X), M.sin(pi * Y), M.sin(pi * Z)
+    cx, cy, cz = M.cos(pi * X), M.cos(pi * Y), M.cos(pi * Z)
+    u = sx * sy * sz
+    grad = [pi * cx * sy * sz, pi * sx * cy * sz, pi * sx * sy * cz]
+    b = [1.0 + X, 1.0 + Y, 1.0 + Z]
+    conv = b[0] * grad[0] + b[1] * grad[1] + b[2] * grad[2]
+    c = 3.0 + X * Y * Z
+    f = 0.01 * 3.0 * pi ** 2 * u + conv + c * u
+    return M.PdeCoefficients(diffusion=M.isotropic_diffusion(0.01, 3), advection=M.VectorField(b),
+                             reaction=M.ScalarField(c), source=M.ScalarField(f),
+                             dirichlet_data=M.ScalarField(u))
+
+
+def sine_dirichlet(dim=2):
+    """2D analogue: ADR with Dirichlet data sin(pi x) sin(pi y) (vanishing on
+    the unit square's boundary up to rounding) and a variable source."""
+    pi = np.pi
+    u = M.sin(pi * X) * M.sin(pi * Y)
+    return M.PdeCoefficients(diffusion=M.isotropic_diffusion(0.01, 2), advection=M.VectorField([1.0 + X, 1.0 + Y]),
+                             reaction=M.ScalarField(3.0 + X * Y), source=M.ScalarField(2.0 * pi ** 2 * u + 1.0),
+                             dirichlet_data=M.ScalarField(u))
+
+
 def anisotropic(dim):
     """Full variable symmetric tensor + Neumann data (exercises the FULL path)."""
     if dim == 2:

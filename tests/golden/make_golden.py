@@ -65,6 +65,14 @@ def ref_coeffs(name: str, dim: int):
         vec = [1.0, 0.5] + ([0.25] if dim == 3 else [])
         return Rm.PdeCoefficients(advection=Rm.constant_vector(vec), reaction=Rm.constant_scalar(1.0),
                                   source=lambda p: 1.0 + p[:, 0], dirichlet_data=lambda p: p[:, 1])
+    if name == "advdiff3d":  # the reference's own named problem, unmodified
+        return Rm.advection_diffusion_3d_problem()
+    if name == "sine_dirichlet":
+        def u(p):
+            return np.sin(pi * p[:, 0]) * np.sin(pi * p[:, 1])
+        return Rm.PdeCoefficients(diffusion=Rm.isotropic_diffusion(0.01, 2), advection=lambda p: 1.0 + p[:, :2],
+                                  reaction=lambda p: 3.0 + p[:, 0] * p[:, 1],
+                                  source=lambda p: 2.0 * pi ** 2 * u(p) + 1.0, dirichlet_data=u)
     raise KeyError(name)
 
 
@@ -76,7 +84,12 @@ def cases():
     from paper_2007_04881_b200.meshgen import voronoi_simplicial
 
     vb, va = voronoi_simplicial(120, seed=7)
+    v1k, a1k = voronoi_simplicial(1000, seed=0)  # the cfg1 mesh (problems.WORKLOADS["cfg1"])
+    c4 = F.cube_grid(4)
     return [
+        ("cfg1_voronoi1000_poisson_p1", v1k, a1k, 1, "poisson_sine"),
+        ("cube4_advdiff3d_p2", c4, F.grown_clusters(c4, 30, seed=5), 2, "advdiff3d"),
+        ("voronoi120_sinedir_p3", vb, va, 3, "sine_dirichlet"),
         ("clusters10_generic_p2", g10, F.grown_clusters(g10, 23, seed=2), 2, "generic"),
         ("clusters6_poisson_p3", g6, F.grown_clusters(g6, 7, seed=1), 3, "poisson_sine"),
         ("blocks8_vardiff_p2", F.square_grid(8), F.square_blocks(8, 2), 2, "variable_diffusion"),
@@ -88,8 +101,10 @@ def cases():
     ]
 
 
-def main():
+def main(only=None):
     for name, base, agg, p, cname in cases():
+        if only and name not in only:
+            continue
         pm = RM.agglomerate(RM.SimplicialMesh(base.dim, base.vertices, base.simplices), agg)
         C = ref_coeffs(cname, base.dim)
         Rm.classify_boundary_faces(pm, C)
@@ -102,4 +117,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

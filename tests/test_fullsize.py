@@ -6,7 +6,7 @@ rows for those elements (values <= 1e-12 relative per block, columns and
 RHS segments), plus the size-independent invariants of the whole CSR
 (row_ptr = element row-length prefix, strictly increasing columns).
 
-Sizes: cfg1 1k, cfg2 100k, cfg3 250k, cfg4 207k (3D), cfg5 4M cells."""
+Sizes: cfg1 1k, cfg2 100k, cfg3 250k (p = 2..6), cfg4 207k (3D), cfg5 4M cells."""
 
 import numpy as np
 import pytest
@@ -37,7 +37,7 @@ def _faces_index(flat, els):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3p2", "cfg3p3", "cfg3", "cfg3p5", "cfg3p6", "cfg4", "cfg5"])
 def test_fullsize_sampled_rows_against_oracle(cfg):
     import torch
 
@@ -65,7 +65,7 @@ def test_fullsize_sampled_rows_against_oracle(cfg):
     row_len = plan.t["row_len"].cpu().numpy()
     assert np.array_equal(lens, np.repeat(row_len, counts))
 
-    els = _sample(flat, 48 if cfg != "cfg5" else 32, seed=int(cfg[-1]))
+    els = _sample(flat, 48 if cfg != "cfg5" else 32, seed=int(cfg[3]) * 10 + w.degree)
     O._FACE_INDEX[id(pm)] = (pm, _faces_index(flat, els))
     # oracle problem from the spec arrays (no per-element Python objects for 4M cells)
     prob = O.Problem.__new__(O.Problem)
