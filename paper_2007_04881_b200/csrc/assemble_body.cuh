@@ -50,9 +50,6 @@ namespace pdg {
 // unroll factors of the k-step loops (tuning knobs, PDG_JIT_DEFINES)
 #define PDG_STR_(x) #x
 #define PDG_UNROLL(n) _Pragma(PDG_STR_(unroll n))
-#ifndef PDG_VOL_ORDER
-#define PDG_VOL_ORDER 1
-#endif
 #ifndef PDG_VOL_UNROLL
 #define PDG_VOL_UNROLL 1
 #endif
@@ -372,95 +369,11 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           Tab<DIM, P> tb;
           tb.load(bx, x);
           double* col = buf + lane;
-#if PDG_VOL_ORDER
-          // the RHS and the value rows first, the (in-place) sqrt-weighted
-          // gradient rows last: one Tab live at a time (fewer registers)
-          if (cf.has_src()) {
-            const double wf = w * cf.f(x);
-            // phi_f = X_a Y_b (Z_c): fold w f into the x-factors once (P+1 products
-            // instead of one per function)
-            constexpr MultiIdx<DIM, P> mi{};
-            double wx[P + 1];
-#pragma unroll
-            for (int k = 0; k <= P; ++k) wx[k] = wf * tb.v1[0][k];
-#pragma unroll
-            for (int f = 0; f < NB; ++f) {
-              double v = wx[mi.a[f][0]] * tb.v1[1][mi.a[f][1]];
-              if (DIM == 3) v *= tb.v1[2][mi.a[f][2]];
-              rhs_add(f, v);
-            }
-          }
-          if (has_vr) {
-            sc2[lane] = w;
-            double bvec[DIM];
-#pragma unroll
-            for (int i = 0; i < DIM; ++i) bvec[i] = cf.has_adv() ? cf.b_i(i, x) : 0.0;
-            const double cr = cf.has_reac() ? cf.c(x) : 0.0;
-#pragma unroll
-            for (int f = 0; f < NBP; ++f) {
-              double vv = 0.0, rr = 0.0;
-              if (f < NB) {
-                vv = tb.val(f);
-                if (cf.has_adv()) {
-#pragma unroll
-                  for (int i = 0; i < DIM; ++i) rr += bvec[i] * tb.grad(f, i);
-                }
-                if (cf.has_reac()) rr += cr * vv;
-              }
-              col[(rV * NBP + f) * kvp] = vv;
-              col[(rR * NBP + f) * kvp] = rr;
-            }
-          }
           if (nG && sqrtw) {
             const double av = cf.a_iso(x);
             if (av < 0.0) raise_flag(a.flags, PDG_FLAG_NEG_DIFFUSION);
             const double sw = RV.sw[r0 + kq] * fr[DIM + DIM * DIM + 1] * sqrt(fmax(av, 0.0)) * valid;
-#if PDG_VOL_ORDER
-            Tab<DIM, P>& ts = tb;  // last use of tb: scale in place (one table live)
-#else
             Tab<DIM, P> ts = tb;
-#endif
-            ts.scale(sw);
-#pragma unroll
-            for (int c = 0; c < DIM; ++c)
-#pragma unroll
-              for (int f = 0; f < NBP; ++f) col[(c * NBP + f) * kvp] = f < NB ? ts.grad(f, c) : 0.0;
-          } else if (nG) {
-            const double av = dk == PDG_DIFF_ISO ? cf.a_iso(x) : 1.0;
-            sc1[lane] = w * av;
-#pragma unroll
-            for (int c = 0; c < DIM; ++c)
-#pragma unroll
-              for (int f = 0; f < NBP; ++f) col[(c * NBP + f) * kvp] = f < NB ? tb.grad(f, c) : 0.0;
-            if (full) {
-              double A[DIM][DIM];
-#pragma unroll
-              for (int i = 0; i < DIM; ++i)
-#pragma unroll
-                for (int j = 0; j < DIM; ++j) A[i][j] = cf.a_ij(i, j, x);
-#pragma unroll
-              for (int c = 0; c < DIM; ++c)
-#pragma unroll
-                for (int f = 0; f < NBP; ++f) {
-                  double v = 0.0;
-                  if (f < NB) {
-#pragma unroll
-                    for (int j = 0; j < DIM; ++j) v += A[c][j] * tb.grad(f, j);
-                  }
-                  col[((rAG + c) * NBP + f) * kvp] = v;
-                }
-            }
-          }
-#else
-          if (nG && sqrtw) {
-            const double av = cf.a_iso(x);
-            if (av < 0.0) raise_flag(a.flags, PDG_FLAG_NEG_DIFFUSION);
-            const double sw = RV.sw[r0 + kq] * fr[DIM + DIM * DIM + 1] * sqrt(fmax(av, 0.0)) * valid;
-#if PDG_VOL_ORDER
-            Tab<DIM, P>& ts = tb;  // last use of tb: scale in place (one table live)
-#else
-            Tab<DIM, P> ts = tb;
-#endif
             ts.scale(sw);
 #pragma unroll
             for (int c = 0; c < DIM; ++c)
@@ -528,7 +441,6 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
               rhs_add(f, v);
             }
           }
-#endif
         }
         __syncwarp();
         PDG_T(1)

@@ -96,15 +96,21 @@ def _flow_side(plan, fid: int) -> int:
     sigma = torch.empty(max(f.n_faces, 1), dtype=torch.float64, device=dev)
     flow = torch.empty(max(f.n_faces, 1), dtype=torch.int8, device=dev)
     abar = torch.empty(max(f.n_elements, 1), dtype=torch.float64, device=dev)
+    # polydg classifies the face whatever its tag (elemental_inflow_part,
+    # model.py:176-191): the pre-pass sees every boundary face as Dirichlet
+    tags = torch.from_numpy(np.where(f.face_neighbor == BOUNDARY, TAG_CODE["dirichlet"], TAG_CODE["interior"])
+                            .astype(np.int8) if f.n_faces else np.zeros(1, np.int8)).to(dev)
+    m = _lib.Mesh.from_buffer_copy(plan.dm.struct)
+    m.face_tag = _lib.ptr(tags)
     plan.flags.zero_()
-    _lib.check(plan.lib.pdg_frames_build(C.byref(plan.dm.struct), C.byref(plan.basis), C.byref(plan.frames),
+    _lib.check(plan.lib.pdg_frames_build(C.byref(m), C.byref(plan.basis), C.byref(plan.frames),
                                          _lib.ptr(plan.flags), _lib.stream_ptr(plan.stream)))
-    _lib.check(plan.lib.pdg_face_prepass(C.byref(plan.dm.struct), C.byref(plan.basis), C.byref(plan.coeffs),
+    _lib.check(plan.lib.pdg_face_prepass(C.byref(m), C.byref(plan.basis), C.byref(plan.coeffs),
                                          C.byref(plan.rules.struct), C.byref(plan.params), _lib.ptr(sigma),
                                          _lib.ptr(flow), _lib.ptr(abar), _lib.ptr(plan.flags),
                                          _lib.stream_ptr(plan.stream)))
     plan.stream.synchronize()
-    _raise_flags(int(plan.flags.item()) & ~_lib.FLAG_UNCLASSIFIED)
+    _raise_flags(int(plan.flags.item()) & ~_lib.FLAG_NEG_DIFFUSION)
     return int(flow[fid].item())
 
 
@@ -279,7 +285,9 @@ def face_sigma(mesh, coeffs, specs, config=None):
     """Penalty sigma and flow side of every face from the device pre-pass
     (polydg ``MeshGeometry.face_sigma`` / ``upwind_side`` / ``dirichlet_inflow``,
     assembly.py:596-626) -> (sigma [n_faces], flow [n_faces]); flow: interior
-    0 = owner inflow, 1 = neighbour inflow, -1 = none; boundary 1 = owner inflow."""
+    0 = owner inflow, 1 = neighbour inflow, -1 = none; boundary 1 = owner inflow.
+    As in polydg's work plan, sigma and flow are formed only where the
+    assembly reads them (interior and Dirichlet faces); other faces hold 0."""
     import torch
 
     from .assembly import AssemblyConfig, SipgPlan
