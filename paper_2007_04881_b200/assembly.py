@@ -548,6 +548,9 @@ class SipgPlan:
     def _elements(self, write_col_idx=True):
         import ctypes as C
 
+        if os.environ.get("PDG_SKIP_COLS") == "1":  # ablation knob (measurement only: col_idx left unwritten)
+            write_col_idx = False
+
         tail = (C.byref(self.rules.struct), C.byref(self.params), C.byref(self.pattern),
                 C.byref(self.frames), _lib.ptr(self.t["sigma"]), _lib.ptr(self.t["flow"]),
                 _lib.ptr(self.t["values"]), 1 if write_col_idx else 0, _lib.ptr(self.t["rhs"]),

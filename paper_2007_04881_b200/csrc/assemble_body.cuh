@@ -69,6 +69,22 @@ namespace pdg {
   }
 
 
+// result stores (values, col_idx) are written once and never re-read by the
+// kernel: streaming (evict-first) stores keep L2 for the frames / records the
+// neighbouring warps re-read (same-box A/B r02, 400k cfg5 cells: 6.50 vs
+// 6.55 ms; 32-bit offsets inside the row block were slower, 6.77 ms)
+#ifndef PDG_ST_CS
+#define PDG_ST_CS 1
+#endif
+template <class T>
+__device__ __forceinline__ void st_out(T* p, T v) {
+#if PDG_ST_CS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
 constexpr int NBR_WIN = 16;  // neighbour entries staged per window
@@ -166,6 +182,31 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Bulk asynchronous copies (TMA engine, SASS UBLKCP) completing on a per-warp
+// mbarrier: the next element's interface-record window and simplex frames are
+// two contiguous runs, so one elected lane moves them with two instructions
+// instead of 32 lanes issuing 16-byte LDGSTS (same-box A/B r02, 400k cfg5
+// cells: 6.22 vs 6.28 ms with LDGSTS; PDG_BULK=0 restores the LDGSTS path).
+#ifndef PDG_BULK
+#define PDG_BULK 1
+#endif
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* mb) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mb)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t phase) {
+  asm volatile("{\n .reg .pred p;\n PDG_MBW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra PDG_MBW_%=;\n}\n" ::"r"(smem_u32(mb)), "r"(phase) : "memory");
+}
+
 template <int DIM>
 __device__ __forceinline__ BoxConst<DIM> load_box(const double* erec, int64_t e) {
   const double* r = erec + e * Widths<DIM>::ER;
@@ -192,8 +233,8 @@ __device__ __forceinline__ void store_block(double* values, int64_t voff, int64_
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int i = r * 8 + g, j = cc * 8 + 2 * t + u;
-        if (i < ne && j < nj) values[voff + (int64_t)i * L + col0 + j] = c[r][cc][u];
-        if (SYM && cc > r && j < ne && i < nj) values[voff + (int64_t)j * L + col0 + i] = c[r][cc][u];
+        if (i < ne && j < nj) st_out(values + voff + (int64_t)i * L + col0 + j, c[r][cc][u]);
+        if (SYM && cc > r && j < ne && i < nj) st_out(values + voff + (int64_t)j * L + col0 + i, c[r][cc][u]);
       }
     }
   }
@@ -257,6 +298,14 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   // the L2 load of the record overlaps the paired round's tabulation)
   constexpr bool STAGE_BOX = DIM == 3;
   double* ebx = ffr + NBR_WIN * W::FF;
+  // per-warp mbarrier of the bulk copies (last 2 doubles of the warp's region)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(buf + a.lay.warp_doubles - 2);
+  const bool bulk = PDG_BULK && !a.mode;
+  uint32_t mphase = 0;
+  if (bulk) {
+    if (lane == 0) mbar_init(mbar);
+    __syncwarp();
+  }
 
   const int kv = KV ? KV : a.lay.kv, kvp = kv + 4;
   const int dk = cf.diff_kind();
@@ -280,6 +329,22 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   auto issue_next = [&](int64_t kk, int rb) -> bool {
     if (kk >= pat.n_row_elements) return false;
     const int32_t en = pat.row_elements ? pat.row_elements[kk] : (int32_t)kk;
+    if (bulk) {  // two bulk copies by one lane, completion on the warp's mbarrier
+      const int64_t r0n = pat.nbr_ptr[en];
+      const int nwn = min(NBR_WIN, (int)(pat.nbr_ptr[en + 1] - r0n));
+      const int64_t s0n = m.elem_ptr[en];
+      const int nsn = (int)(m.elem_ptr[en + 1] - s0n);
+      const bool frames = nsn <= FR_MAX;
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads before async writes
+        const uint32_t rbytes = (uint32_t)nwn * (uint32_t)sizeof(pdg_iface_rec);
+        const uint32_t fbytes = frames ? (uint32_t)nsn * W::SF * 8u : 0u;
+        mbar_expect_tx(mbar, rbytes + fbytes);
+        bulk_g2s(recs + rb * NBR_WIN, pat.nbr_rec + r0n, rbytes, mbar);
+        if (frames) bulk_g2s(sfr, a.sframe + s0n * W::SF, fbytes, mbar);
+      }
+      return frames;
+    }
     if (!mode) {
       const int64_t r0n = pat.nbr_ptr[en];
       const int nwn = min(NBR_WIN, (int)(pat.nbr_ptr[en + 1] - r0n));
@@ -312,12 +377,16 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   int rb = 0;
   bool next_frames = issue_next(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, rb);
   cp_async_commit();
-  long long tacc[PDG_TIMERS ? 9 : 1] = {0};
+  long long tacc[PDG_TIMERS ? 10 : 1] = {0};
   long long tprev = PDG_TIMERS ? clock64() : 0;
   int nel_done = 0;
   for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < pat.n_row_elements;
        k += nwarps, rb ^= 1) {
     const bool fr_smem = next_frames;
+    if (bulk) {
+      mbar_wait(mbar, mphase);
+      mphase ^= 1u;
+    }
     cp_async_wait_all();
     __syncwarp();
     const int32_t e = pat.row_elements ? pat.row_elements[k] : (int32_t)k;
@@ -511,6 +580,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
     __syncwarp();
     next_frames = issue_next(k + nwarps, rb ^ 1);
     cp_async_commit();
+    __syncwarp();
 
     // ------------------------------------------------------------ interfaces
     // Neighbour entries are staged NBR_WIN at a time as interface records
@@ -639,7 +709,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       const int nw = min(NBR_WIN, nnb - w0);
       if (w0 == 0) {
         // this element's facet frames; the next element's copies stay in flight
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        if (bulk) cp_async_wait_all();  // (the next element's copies are on the mbarrier)
+        else asm volatile("cp.async.wait_group 1;" ::: "memory");
       } else {
         // windows beyond the first (more than NBR_WIN neighbours): synchronous restage
         __syncwarp();
@@ -667,7 +738,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           const int64_t cv = rc[q].dof + (p - rc[q].col);
           int64_t* dst = pat.col_idx + voff + p;
 #pragma unroll 4
-          for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
+          for (int r = 0; r < ne; ++r) st_out<int64_t>(dst + (int64_t)r * Lrow, cv);
         }
       }
       PDG_T(4)
@@ -679,12 +750,16 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         }
         int qb = qi + 1;
         if (qb < nw && rc[qb].j == e) ++qb;
-        const bool pair = (rc[qi].info & 4) && qb < nw && (rc[qb].info & 4);
+        // a single-facet interface takes a paired round, with a partner when
+        // the next one qualifies too, else alone (its half of the slots idle;
+        // cheaper than the general path: staged frames, one contraction)
+        const bool pair = (rc[qi].info & 4) != 0;
+        const bool has_b = qb < nw && (rc[qb].info & 4);
         double co[NT][NT][2];
         zero_tiles<NT>(co);
         if (pair) {
           // ---- two single-facet interfaces in one round
-          const int seg = slot >> 3, ls = slot & 7;
+          const int seg = (slot >> 3) & (has_b ? 1 : 0), ls = slot & 7;
           const int q = seg ? qb : qi;
           const int info = rc[q].info;
           const int pj = rc[q].pj;
@@ -694,18 +769,20 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 #pragma unroll
           for (int i = 0; i < DIM; ++i) nrm[i] = rc[q].nrm[i];
           const BoxConst<DIM> bo = STAGE_BOX ? load_box<DIM>(ebx, q) : load_box<DIM>(a.erec, rc[q].j);
-          tab_slot(nrm, ffr + q * W::FF, r0, min(ls, nq - 1), ls < nq ? 1.0 : 0.0, rc[q].sig,
-                   (info & 1) ? -1.0 : 1.0, (info & 2) != 0, bo);
+          tab_slot(nrm, ffr + q * W::FF, r0, min(ls, nq - 1), (ls < nq && (has_b || slot < 8)) ? 1.0 : 0.0,
+                   rc[q].sig, (info & 1) ? -1.0 : 1.0, (info & 2) != 0, bo);
           __syncwarp();
           PDG_T(5)
           face_contract(0, 2, co);
           store_block<NT, false>(a.values, voff, Lrow, rc[qi].col, ne, rc[qi].nj, co, g, t);
-          zero_tiles<NT>(co);
-          face_contract(2, 4, co);
-          store_block<NT, false>(a.values, voff, Lrow, rc[qb].col, ne, rc[qb].nj, co, g, t);
+          if (has_b) {
+            zero_tiles<NT>(co);
+            face_contract(2, 4, co);
+            store_block<NT, false>(a.values, voff, Lrow, rc[qb].col, ne, rc[qb].nj, co, g, t);
+          }
           __syncwarp();
           PDG_T(6)
-          qi = qb + 1;
+          qi = has_b ? qb + 1 : qi + 1;
           continue;
         }
         // ---- general interface: every face, every sub-facet, rounds of 16 points
@@ -753,6 +830,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           }
         }
         store_block<NT, false>(a.values, voff, Lrow, rc[qi].col, ne, rc[qi].nj, co, g, t);
+        PDG_T(9)
         ++qi;
       }
       __syncwarp();
@@ -900,9 +978,9 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   if (PDG_TIMERS && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && threadIdx.x < 64) {
     const double n = nel_done > 0 ? nel_done : 1;
     printf("PDG_TIMERS blk %d warp %d elements %d per-element cycles: start %.0f voltab %.0f volmma %.0f post %.0f "
-           "window %.0f facetab %.0f facemma %.0f boundary %.0f writeout %.0f\n",
+           "window %.0f facetab %.0f facemma %.0f boundary %.0f writeout %.0f general %.0f\n",
            blockIdx.x, threadIdx.x >> 5, nel_done, tacc[0] / n, tacc[1] / n, tacc[2] / n, tacc[3] / n, tacc[4] / n,
-           tacc[5] / n, tacc[6] / n, tacc[7] / n, tacc[8] / n);
+           tacc[5] / n, tacc[6] / n, tacc[7] / n, tacc[8] / n, tacc[9] / n);
   }
 }
 
