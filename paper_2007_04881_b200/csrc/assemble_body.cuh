@@ -240,6 +240,33 @@ __device__ __forceinline__ void store_block(double* values, int64_t voff, int64_
   }
 }
 
+// Packed remainder tile of a symmetric 10x10 block (NB = 10: p = 3 in 2D,
+// p = 2 in 3D).  The upper triangle needs the 8x8 tile of functions 0-7 plus
+// 19 pairs involving functions 8, 9; one 8x8 DMMA tile with rows
+// {0..5, 8, 9} and columns {8, 9, 6, 7} covers all of them -- (i, 8|9) for
+// i < 6 and (8|9, 6..9) -- so the block costs 2 DMMAs per k-step instead of
+// the 3 of the padded 16x16 upper triangle.  Columns 4-7 read the zero
+// padding row 10.  Only pairs the main tile does not hold are stored.
+__host__ __device__ constexpr int pk_row(int g) { return g < 6 ? g : g + 2; }
+__host__ __device__ constexpr int pk_col(int g) { return g < 2 ? g + 8 : (g < 4 ? g + 4 : 10); }
+
+template <int DIM, int P, bool SYM>
+struct PackPlan {
+  static constexpr bool on = SYM && binom(P + DIM, DIM) == 10;
+};
+
+__device__ __forceinline__ void store_packed10(double* values, int64_t voff, int64_t L, int64_t col0, int ne,
+                                               const double (&c)[2], int g, int t) {
+  const int i = pk_row(g);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int j = pk_col(2 * t + u);
+    if (j >= 10 || (i < 8 && j < 8) || i >= ne || j >= ne) continue;
+    st_out(values + voff + (int64_t)i * L + col0 + j, c[u]);
+    if (!(i >= 8 && j >= 8)) st_out(values + voff + (int64_t)j * L + col0 + i, c[u]);
+  }
+}
+
 template <int NT>
 __device__ __forceinline__ void zero_tiles(double (&c)[NT][NT][2]) {
 #pragma unroll
@@ -319,6 +346,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   // weighting, half the fragment loads).  Needs a(x) >= 0; a negative value
   // raises PDG_FLAG_NEG_DIFFUSION and the host re-runs with PDG_OPT_PLAIN_VOLUME.
   const bool sqrtw = dk == PDG_DIFF_ISO && !(a.prm.options & PDG_OPT_PLAIN_VOLUME);
+  constexpr bool PK = PackPlan<DIM, P, SYM>::on;  // packed remainder tile: cd[0][1] holds rows pk_row x cols pk_col
+  const int fA1 = pk_row(g), fB1 = pk_col(g);
   const int mode = a.mode;
 
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -516,7 +545,16 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         const int nk = (nvalid + 3) >> 2;
         auto vol_kstep = [&](int kk) {
           const int q = kk * 4 + t;
-          if (nG && sqrtw) {
+          if (nG && sqrtw && PK) {
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+              const double a0 = buf[(c * NBP + g) * kvp + q];
+              const double a1 = buf[(c * NBP + fA1) * kvp + q];
+              const double b1 = buf[(c * NBP + fB1) * kvp + q];
+              dmma(cd[0][0], a0, a0);
+              dmma(cd[0][1], a1, b1);
+            }
+          } else if (nG && sqrtw) {
 #pragma unroll
             for (int c = 0; c < DIM; ++c) {
               double fr_[NT];
@@ -527,6 +565,18 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 #pragma unroll
                 for (int cc = 0; cc < NT; ++cc)
                   if (!SYM || cc >= r) dmma(cd[r][cc], fr_[r], fr_[cc]);
+            }
+          } else if (nG && PK) {
+            const double s1 = sc1[q];
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+              const double g0 = buf[(c * NBP + g) * kvp + q];
+              const double gA = buf[(c * NBP + fA1) * kvp + q];
+              const double gB = buf[(c * NBP + fB1) * kvp + q];
+              const double r0v = full ? buf[((rAG + c) * NBP + g) * kvp + q] : g0;
+              const double rBv = full ? buf[((rAG + c) * NBP + fB1) * kvp + q] : gB;
+              dmma(cd[0][0], s1 * g0, r0v);
+              dmma(cd[0][1], s1 * gA, rBv);
             }
           } else if (nG) {
             const double s1 = sc1[q];
@@ -546,7 +596,11 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
                   if (!SYM || cc >= r) dmma(cd[r][cc], lf[r], rf[cc]);
             }
           }
-          if (has_vr) {
+          if (has_vr && PK) {
+            const double s2 = sc2[q];
+            dmma(cd[0][0], s2 * buf[(rV * NBP + g) * kvp + q], buf[(rR * NBP + g) * kvp + q]);
+            dmma(cd[0][1], s2 * buf[(rV * NBP + fA1) * kvp + q], buf[(rR * NBP + fB1) * kvp + q]);
+          } else if (has_vr) {
             const double s2 = sc2[q];
             double lf[NT], rf[NT];
 #pragma unroll
@@ -690,11 +744,23 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
             l1[i] = al * va[i];
           }
         }
+        if constexpr (PK) {
+          const double vA = buf[(0 * NBP + fA1) * KFP + qq], vB = buf[(0 * NBP + fB1) * KFP + qq];
+          dmma(cd[0][0], l1[0], va[0]);
+          if (grad_terms) {
+            const double fA = buf[(1 * NBP + fA1) * KFP + qq], fB = buf[(1 * NBP + fB1) * KFP + qq];
+            dmma(cd[0][0], l2[0], fa[0]);
+            dmma(cd[0][1], al * vA + be * fA, vB);
+            dmma(cd[0][1], be * vA, fB);
+          } else {
+            dmma(cd[0][1], al * vA, vB);
+          }
+        }
 #pragma unroll
         for (int r = 0; r < NT; ++r)
 #pragma unroll
           for (int cc = 0; cc < NT; ++cc) {
-            if (!SYM || cc >= r) {
+            if (!PK && (!SYM || cc >= r)) {
               dmma(cd[r][cc], l1[r], va[cc]);
               if (grad_terms) dmma(cd[r][cc], l2[r], fa[cc]);
             }
@@ -936,14 +1002,25 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
               l1[i] = al * va[i] + be * fa[i];
               l2[i] = be * va[i];
             }
+            if constexpr (PK) {
+              const double vA = buf[(0 * NBP + fA1) * KFP + qq], vB = buf[(0 * NBP + fB1) * KFP + qq];
+              const double fA = buf[(1 * NBP + fA1) * KFP + qq], fB = buf[(1 * NBP + fB1) * KFP + qq];
+              dmma(cd[0][0], l1[0], va[0]);
+              dmma(cd[0][1], al * vA + be * fA, vB);
+              if (use_f) {
+                dmma(cd[0][0], l2[0], fa[0]);
+                dmma(cd[0][1], be * vA, fB);
+              }
+            } else {
 #pragma unroll
-            for (int r = 0; r < NT; ++r)
+              for (int r = 0; r < NT; ++r)
 #pragma unroll
-              for (int cc = 0; cc < NT; ++cc)
-                if (!SYM || cc >= r) {
-                  dmma(cd[r][cc], l1[r], va[cc]);
-                  if (use_f) dmma(cd[r][cc], l2[r], fa[cc]);
-                }
+                for (int cc = 0; cc < NT; ++cc)
+                  if (!SYM || cc >= r) {
+                    dmma(cd[r][cc], l1[r], va[cc]);
+                    if (use_f) dmma(cd[r][cc], l2[r], fa[cc]);
+                  }
+            }
           }
         }
         __syncwarp();
@@ -952,7 +1029,13 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 
     PDG_T(7)
     // ------------------------------------------------------------ write-out
-    store_block<NT, SYM>(a.values, voff, Lrow, colself, ne, ne, cd, g, t);
+    if constexpr (PK) {
+      double c00[1][1][2] = {{{cd[0][0][0], cd[0][0][1]}}};
+      store_block<1, true>(a.values, voff, Lrow, colself, ne, ne, c00, g, t);
+      store_packed10(a.values, voff, Lrow, colself, ne, cd[0][1], g, t);
+    } else {
+      store_block<NT, SYM>(a.values, voff, Lrow, colself, ne, ne, cd, g, t);
+    }
     double* rhs_out = mode ? a.rhs + k * NB : a.rhs + dof_e;
     __syncwarp();
     if constexpr (S::RHS_REGS) {
