@@ -21,6 +21,7 @@ from __future__ import annotations
 import os
 import time
 import warnings
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -133,24 +134,78 @@ class CSRMatrix:
         return float(np.max(np.abs(self.values - other.values) / denom))
 
 
+class _RaggedSeq(Sequence):
+    """``list[np.ndarray]`` view of a CSR-style ragged array (no per-row objects
+    until a row is read)."""
+
+    def __init__(self, ptr: np.ndarray, data: np.ndarray):
+        self._ptr, self._data = ptr, data
+
+    def __len__(self):
+        return int(self._ptr.shape[0] - 1)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        i = int(i)
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return self._data[self._ptr[i]:self._ptr[i + 1]]
+
+
 @dataclass
 class BlockPattern:
-    """CSR skeleton with one dense block per adjacent element pair."""
+    """CSR skeleton with one dense block per adjacent element pair (polydg
+    ``BlockPattern``, assembly.py:207-272).
+
+    Array-backed: ``neighbors`` / ``col_starts`` are ragged views of two flat
+    arrays (the device adjacency), ``local_block_start`` / ``block_slots``
+    binary-search the ascending ``row_elements`` -- no per-element Python
+    objects, so a 4M-element pattern costs a few vectorised passes."""
 
     dof_map: DofMap
     row_elements: np.ndarray
-    neighbors: list
-    col_starts: list
+    neighbors: Sequence
+    col_starts: Sequence
     row_ptr: np.ndarray
     col_idx: np.ndarray
     global_rows: np.ndarray
-    _row_pos: dict = field(repr=False, default_factory=dict)
 
     def __post_init__(self):
-        self._row_pos = {int(e): k for k, e in enumerate(self.row_elements)}
+        self.row_elements = np.asarray(self.row_elements, dtype=np.int64)
         counts = np.diff(self.dof_map.offsets)[self.row_elements]
         self._row_offsets = np.zeros(len(counts) + 1, dtype=np.int64)
         np.cumsum(counts, out=self._row_offsets[1:])
+
+    @classmethod
+    def from_adjacency(cls, dof_map: DofMap, row_elements, nbr_ptr, nbr_elem, row_ptr, col_idx) -> "BlockPattern":
+        """Pattern of ``row_elements`` from the sorted adjacency (nbr_ptr over
+        all elements, nbr_elem = neighbours incl. self) -- vectorised."""
+        rows = np.asarray(row_elements, dtype=np.int64)
+        a, b = nbr_ptr[rows], nbr_ptr[rows + 1]
+        cnt = (b - a).astype(np.int64)
+        ptr = np.zeros(rows.size + 1, np.int64)
+        np.cumsum(cnt, out=ptr[1:])
+        idx = np.repeat(a - ptr[:-1], cnt) + np.arange(int(ptr[-1]), dtype=np.int64)
+        nbrs = np.asarray(nbr_elem[idx], dtype=np.int64)
+        w = np.diff(dof_map.offsets)[nbrs]
+        cs = np.cumsum(w) - w                         # global running start ...
+        cs -= np.repeat(cs[ptr[:-1]] if rows.size else cs[:0], cnt)  # ... made per-row
+        ne = np.diff(dof_map.offsets)[rows]
+        first = dof_map.offsets[rows]
+        rp = np.zeros(rows.size + 1, np.int64)
+        np.cumsum(ne, out=rp[1:])
+        grows = np.repeat(first - rp[:-1], ne) + np.arange(int(rp[-1]), dtype=np.int64)
+        return cls(dof_map, rows, _RaggedSeq(ptr, nbrs), _RaggedSeq(ptr, cs.astype(np.int64)), row_ptr, col_idx,
+                   grows)
+
+    def _local(self, element: int):
+        k = int(np.searchsorted(self.row_elements, element))
+        if k < self.row_elements.shape[0] and int(self.row_elements[k]) == int(element):
+            return k
+        return None
 
     @property
     def n_local_rows(self) -> int:
@@ -161,10 +216,13 @@ class BlockPattern:
         return int(self.col_idx.shape[0])
 
     def local_block_start(self, element: int) -> int:
-        return self._row_pos[element]
+        k = self._local(element)
+        if k is None:
+            raise KeyError(element)
+        return k
 
     def block_slots(self, row_element: int, col_element: int) -> np.ndarray:
-        local = self._row_pos.get(row_element)
+        local = self._local(row_element)
         if local is None:
             raise PatternMissError(f"element {row_element} owns no rows here")
         nbrs = self.neighbors[local]
@@ -239,6 +297,57 @@ class AssemblyStats:
 # ---------------------------------------------------------------------------
 # device residency
 # ---------------------------------------------------------------------------
+
+_D2H_CHUNK = 1 << 28  # 256 MiB pinned staging buffers
+
+
+def download(t, stream=None, chunk_bytes: int = _D2H_CHUNK) -> np.ndarray:
+    """Device tensor -> new numpy array through two pinned staging buffers:
+    chunk i+1 is copied device->host (DMA) while chunk i is copied into the
+    destination array by a host thread pool (numpy copies release the GIL), so
+    the transfer runs at the link's pinned rate instead of the pageable one."""
+    torch = _torch()
+    t = t.contiguous().reshape(-1)
+    n = int(t.numel())
+    out = np.empty(n, dtype=np.dtype(str(t.dtype).replace("torch.", "")))
+    nbytes = n * t.element_size()
+    if nbytes <= (1 << 24):  # small: one plain copy
+        out[:] = t.cpu().numpy()
+        return out
+    from concurrent.futures import ThreadPoolExecutor
+
+    stream = stream or torch.cuda.current_stream(t.device)
+    per = max(1, chunk_bytes // t.element_size())
+    stages = [torch.empty(per, dtype=t.dtype, pin_memory=True) for _ in range(2)]
+    events = [torch.cuda.Event() for _ in range(2)]
+    nthreads = max(1, min(8, (os.cpu_count() or 2)))
+    pool = ThreadPoolExecutor(nthreads)
+    pending = [None, None]
+
+    def host_copy(buf, a, m):
+        src = buf[:m].numpy()
+        parts = np.linspace(0, m, nthreads + 1).astype(np.int64)
+        list(pool.map(lambda k: np.copyto(out[a + parts[k]:a + parts[k + 1]], src[parts[k]:parts[k + 1]]),
+                      range(nthreads)))
+
+    try:
+        with torch.cuda.stream(stream):
+            for i, a in enumerate(range(0, n, per)):
+                s = i & 1
+                m = min(per, n - a)
+                if pending[s] is not None:
+                    pending[s].result()  # the host copy out of this buffer is done
+                stages[s][:m].copy_(t[a:a + m], non_blocking=True)
+                events[s].record(stream)
+                events[s].synchronize()
+                pending[s] = pool.submit(host_copy, stages[s], a, m)
+        for f in pending:
+            if f is not None:
+                f.result()
+    finally:
+        pool.shutdown(wait=True)
+    return out
+
 
 def _torch():
     import torch
@@ -652,25 +761,20 @@ class SipgPlan:
         return self.t["rhs"][: self.dof.n_dofs]
 
     def to_csr(self) -> CSRMatrix:
-        return CSRMatrix(self.n_local_rows, self.dof.n_dofs, self.row_ptr.cpu().numpy(),
-                         self.col_idx.cpu().numpy(), self.values.cpu().numpy())
+        """The CSR in host memory: pinned, chunked, double-buffered device->host
+        copies into freshly allocated numpy arrays (``download``)."""
+        return CSRMatrix(self.n_local_rows, self.dof.n_dofs, download(self.row_ptr, self.stream),
+                         download(self.col_idx, self.stream), download(self.values, self.stream))
 
-    def block_pattern(self) -> BlockPattern:
-        ptr = self.t["nbr_ptr"].cpu().numpy()
-        nb = self.t["nbr_elem"][: int(ptr[-1])].cpu().numpy().astype(np.int64)
-        counts = np.diff(self.dof.offsets)
-        neighbors, col_starts, grows = [], [], []
-        for e in self.row_elements:
-            ns = nb[ptr[e]:ptr[e + 1]]
-            w = counts[ns]
-            st = np.zeros(ns.shape[0], np.int64)
-            np.cumsum(w[:-1], out=st[1:])
-            neighbors.append(ns)
-            col_starts.append(st)
-            grows.append(np.arange(self.dof.offsets[e], self.dof.offsets[e + 1]))
-        gr = np.concatenate(grows) if grows else np.zeros(0, np.int64)
-        return BlockPattern(self.dof, self.row_elements, neighbors, col_starts,
-                            self.row_ptr.cpu().numpy(), self.col_idx.cpu().numpy(), gr)
+    def block_pattern(self, row_ptr=None, col_idx=None) -> BlockPattern:
+        """polydg BlockPattern of the plan's rows (vectorised from the device
+        adjacency).  ``row_ptr`` / ``col_idx``: host copies already made (the
+        pattern then shares them instead of downloading a second copy)."""
+        ptr = download(self.t["nbr_ptr"], self.stream)
+        nb = download(self.t["nbr_elem"][: int(ptr[-1])], self.stream)
+        return BlockPattern.from_adjacency(self.dof, self.row_elements, ptr, nb,
+                                           row_ptr if row_ptr is not None else download(self.row_ptr, self.stream),
+                                           col_idx if col_idx is not None else download(self.col_idx, self.stream))
 
     def work_stats(self) -> dict:
         """polydg per-kernel work items / nnz_written (assembly.py:360-391)."""
@@ -849,8 +953,11 @@ def assemble_approach2(mesh, coeffs, specs, config: Optional[AssemblyConfig] = N
     res = assemble_device(mesh, coeffs, specs, config)
     plan = res.plan
     matrix = plan.to_csr()
-    rhs = plan.rhs.cpu().numpy().copy()
-    pattern = plan.block_pattern()
+    rhs = download(plan.rhs, plan.stream)
+    # polydg's pattern owns its own copy of row_ptr / col_idx (empty_matrix
+    # copies again); here it shares the matrix's host arrays instead of a second
+    # 8 B/nnz download
+    pattern = plan.block_pattern(matrix.row_ptr, matrix.col_idx)
     res.stats.total_seconds = time.perf_counter() - t0
     return matrix, rhs, res.stats, pattern
 

@@ -289,3 +289,28 @@ def test_element_kernel_mass_identity_on_box():
         spec = build_basis(pm, p)[0]
         K, _ = element_kernel(pm, 0, coeffs, spec)
         np.testing.assert_allclose(K, np.eye(spec.n_funcs), atol=1e-12)
+
+
+def test_pinned_chunked_download_and_block_slots_on_assembled_matrix():
+    """download() (pinned double-buffered D2H into numpy) is exact for odd
+    chunkings; the pattern's block_slots address the assembled values."""
+    import torch
+
+    from paper_2007_04881_b200.assembly import download
+
+    t = torch.randn(3_000_001, dtype=torch.float64, device="cuda")
+    for ch in (1 << 20, 3 << 19, 1 << 30):
+        assert np.array_equal(download(t, chunk_bytes=ch), t.cpu().numpy())
+    ti = torch.randint(0, 1 << 40, (2_500_003,), dtype=torch.int64, device="cuda")
+    assert np.array_equal(download(ti, chunk_bytes=1 << 20), ti.cpu().numpy())
+    pm = _mesh("clusters10")
+    coeffs = F.generic(2)
+    classify_boundary_faces(pm, coeffs)
+    specs = build_basis(pm, 2)
+    m, _, _, pattern = assemble_approach2(pm, coeffs, specs)
+    dense = m.to_dense()
+    off = pattern.dof_map.offsets
+    for k, e in enumerate(pattern.row_elements[:12]):
+        for j in pattern.neighbors[k]:
+            sl = pattern.block_slots(int(e), int(j))
+            assert np.array_equal(m.values[sl], dense[off[e]:off[e + 1], off[j]:off[j + 1]])

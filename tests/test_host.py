@@ -314,3 +314,42 @@ def test_submesh_rows_bit_identical_3d_variable_degree_coverable():
     cov = np.arange(pm.n_elements) % 3 == 0
     _local_rows_equal_global(pm, coeffs, build_basis(pm, deg), 2,
                              AssemblyConfig(penalty=PenaltyConfig(constant=9.0, coverable=cov)))
+
+
+def test_block_pattern_from_adjacency_matches_per_element_build():
+    """Vectorised BlockPattern (ragged views of the device adjacency) equals the
+    per-element construction of polydg (assembly.py:207-272); block_slots
+    addresses the CSR exactly and misses raise PatternMissError."""
+    from paper_2007_04881_b200.assembly import BlockPattern, DofMap, PatternMissError
+
+    rng = np.random.default_rng(0)
+    nel = 40
+    deg = rng.integers(0, 4, nel)
+    counts = np.array([(p + 1) * (p + 2) // 2 for p in deg], np.int64)
+    dm = DofMap(np.concatenate([[0], np.cumsum(counts)]).astype(np.int64))
+    adj = [sorted({e} | set(rng.choice(nel, rng.integers(1, 6), replace=False).tolist())) for e in range(nel)]
+    nbr_ptr = np.concatenate([[0], np.cumsum([len(a) for a in adj])]).astype(np.int64)
+    nbr_elem = np.concatenate(adj).astype(np.int32)
+    rows = np.array([1, 4, 5, 17, 39])
+    lens = np.concatenate([np.full(counts[e], counts[adj[e]].sum()) for e in rows])
+    row_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col_idx = np.concatenate([np.tile(np.concatenate([np.arange(dm.offsets[j], dm.offsets[j + 1])
+                                                      for j in adj[e]]), counts[e]) for e in rows])
+    bp = BlockPattern.from_adjacency(dm, rows, nbr_ptr, nbr_elem, row_ptr, col_idx)
+    assert len(bp.neighbors) == rows.size and bp.nnz == col_idx.size
+    for k, e in enumerate(rows):
+        assert np.array_equal(bp.neighbors[k], adj[e])
+        st = np.concatenate([[0], np.cumsum(counts[adj[e]])[:-1]])
+        assert np.array_equal(bp.col_starts[k], st)
+        assert bp.local_block_start(int(e)) == k
+        for j in adj[e]:
+            slots = bp.block_slots(int(e), int(j))
+            assert np.array_equal(col_idx[slots], np.broadcast_to(np.arange(dm.offsets[j], dm.offsets[j + 1]),
+                                                                  slots.shape))
+    assert np.array_equal(bp.global_rows, np.concatenate([np.arange(dm.offsets[e], dm.offsets[e + 1])
+                                                          for e in rows]))
+    with pytest.raises(PatternMissError):
+        bp.block_slots(2, 2)
+    missing = next(j for j in range(nel) if j not in adj[4])
+    with pytest.raises(PatternMissError):
+        bp.block_slots(4, missing)
