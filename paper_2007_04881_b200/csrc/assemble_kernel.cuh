@@ -3,6 +3,8 @@
 // from the same body (assemble_body.cuh).
 #pragma once
 
+#include <cstdlib>
+
 #include "assemble_body.cuh"
 #include "pdg_internal.cuh"
 
@@ -21,7 +23,17 @@ inline AsmLayout make_layout(int dim, int P, int diff_kind, bool has_vr, int rhs
   const int nVR = has_vr ? 2 : 0;
   L.vrows = nG + nAG + nVR;
   if (L.vrows == 0) L.vrows = 1;
+  // volume slots per round: 32 while the table stays under 20 KB per warp;
+  // PDG_VOL_KV=16|32 forces one (tuning knob: smaller tables raise occupancy)
   L.kv = (L.vrows * NBP * 36 * 8 <= 20 * 1024) ? 32 : 16;
+  // 10-function bases with the advection/reaction rows: 16 slots keep 3 CTAs
+  // per SM (shared memory) -- same-box r02, 250k cfg3 p=3: 4.37 vs 4.58 ms
+  // (p = 2 and p = 4 measured better at 32)
+  if (NB == 10 && L.vrows >= 4) L.kv = 16;
+  if (const char* v = getenv("PDG_VOL_KV")) {
+    const int kv = atoi(v);
+    if (kv == 16 || kv == 32) L.kv = kv;
+  }
   const int vol = L.vrows * NBP * (L.kv + 4);
   const int face = 4 * NBP * KFP;
   const int red = 32 * NB;

@@ -59,7 +59,7 @@ def _mesh(name):
 
 
 @pytest.mark.parametrize("name,p", [("blocks8", 1), ("clusters6", 2), ("zigzag", 2), ("cube", 1),
-                                    ("identity4", 1), ("cube3", 2)])
+                                    ("identity4", 1), ("cube3", 2), ("clusters10", 3)])
 def test_cross_oracle_generic(name, p):
     """The reference suite's cross-oracle cases (test_assembly.py:349-389)."""
     pm = _mesh(name)
@@ -112,7 +112,7 @@ def test_anisotropic_tensor_with_neumann(name, p):
     _run(pm, F.anisotropic(pm.dim), p, predicate=lambda x: x[0] < 0.5)
 
 
-@pytest.mark.parametrize("name,p", [("clusters10", 2), ("cube3", 1)])
+@pytest.mark.parametrize("name,p", [("clusters10", 2), ("clusters10", 3), ("cube3", 1), ("cube3", 2)])
 def test_hyperbolic_inflow_outflow(name, p):
     pm = _mesh(name)
     _run(pm, F.hyperbolic(pm.dim), p)
