@@ -1038,7 +1038,27 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
     }
     double* rhs_out = mode ? a.rhs + k * NB : a.rhs + dof_e;
     __syncwarp();
-    if constexpr (S::RHS_REGS) {
+    if constexpr (S::RHS_REGS && NB <= 16) {
+      // transpose-reduce across the warp: four halving exchanges (lane bits
+      // 16, 8, 4, 2) leave each lane one function's partial over 16 lanes, the
+      // last exchange (bit 1) completes it -- 16 shuffles, no shared memory
+      double v[16];
+#pragma unroll
+      for (int f = 0; f < 16; ++f) v[f] = f < NB ? racc[f] : 0.0;
+#pragma unroll
+      for (int w = 8, bit = 16; w >= 1; w >>= 1, bit >>= 1) {
+        const bool hi = (lane & bit) != 0;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+          const double send = hi ? v[i] : v[i + w];
+          const double keep = hi ? v[i + w] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+        }
+      }
+      const double tot = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+      const int f = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+      if (!(lane & 1) && f < ne) rhs_out[f] = tot;
+    } else if constexpr (S::RHS_REGS) {
 #pragma unroll
       for (int f = 0; f < NB; ++f) buf[lane * NB + f] = racc[f];
       __syncwarp();
