@@ -151,15 +151,21 @@ class ClockSampler:
 
 
 def fp64_peak():
-    """Measured FP64 (DMMA/DFMA) peak, TFLOP/s: profiles/fp64_peaks_r01.json
-    (MEASURED_PEAKS.json carries no fp64 figure)."""
-    p = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
-    try:
-        with open(p) as fh:
-            d = json.load(fh)
-        return float(max(d["dmma_m8n8k4_acc4_tflops"], d["dfma_tflops"])), "profiles/fp64_peaks_r01.json (measured)"
-    except Exception:
-        return 37.0, "B200 datasheet fallback"
+    """Builder-measured FP64 (DMMA/DFMA) peak, TFLOP/s, newest of
+    profiles/fp64_peaks_r0*.json (tools/fp64_peaks.cu; MEASURED_PEAKS.json
+    carries no fp64 figure)."""
+    for name in ("fp64_peaks_r02.json", "fp64_peaks_r01.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        try:
+            with open(p) as fh:
+                d = json.load(fh)
+            mhz = d.get("clocks", {}).get("sm_mhz_median") or d.get("clock_khz_attr", 0) / 1000
+            return (float(max(d["dmma_m8n8k4_acc4_tflops"], d["dfma_tflops"])),
+                    f"profiles/{name} (builder-measured fp64: DMMA m8n8k4 / DFMA microbenchmark, "
+                    f"{mhz:.0f} MHz SM clock)")
+        except Exception:
+            continue
+    return 37.0, "B200 datasheet fallback"
 
 
 def hbm_peak():
