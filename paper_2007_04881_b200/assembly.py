@@ -314,14 +314,11 @@ def download(t, stream=None, chunk_bytes: int = _D2H_CHUNK) -> np.ndarray:
     if nbytes <= (1 << 24):  # small: one plain copy
         out[:] = t.cpu().numpy()
         return out
-    from concurrent.futures import ThreadPoolExecutor
-
     stream = stream or torch.cuda.current_stream(t.device)
     per = max(1, chunk_bytes // t.element_size())
-    stages = [torch.empty(per, dtype=t.dtype, pin_memory=True) for _ in range(2)]
+    raw, pool, nthreads = _staging(per * t.element_size())
+    stages = [r[: per * t.element_size()].view(t.dtype) for r in raw]
     events = [torch.cuda.Event() for _ in range(2)]
-    nthreads = max(1, min(8, (os.cpu_count() or 2)))
-    pool = ThreadPoolExecutor(nthreads)
     pending = [None, None]
 
     def host_copy(buf, a, m):
@@ -341,12 +338,31 @@ def download(t, stream=None, chunk_bytes: int = _D2H_CHUNK) -> np.ndarray:
                 events[s].record(stream)
                 events[s].synchronize()
                 pending[s] = pool.submit(host_copy, stages[s], a, m)
+    finally:
         for f in pending:
             if f is not None:
                 f.result()
-    finally:
-        pool.shutdown(wait=True)
     return out
+
+
+_STAGING = {}
+
+
+def _staging(nbytes: int):
+    """Two pinned staging buffers of at least ``nbytes`` and the host copy
+    pool, allocated once per process (pinned allocations cost milliseconds)."""
+    torch = _torch()
+    cur = _STAGING.get("raw")
+    if cur is None or cur[0].numel() < nbytes:
+        _STAGING["raw"] = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    if "pool" not in _STAGING:
+        from concurrent.futures import ThreadPoolExecutor
+
+        n = max(1, min(8, (os.cpu_count() or 2)))
+        # two submitters (the staging buffers) + n copy workers
+        _STAGING["pool"] = (ThreadPoolExecutor(n + 2), n)
+    pool, n = _STAGING["pool"]
+    return _STAGING["raw"], pool, n
 
 
 def _torch():

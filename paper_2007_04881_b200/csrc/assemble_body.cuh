@@ -184,11 +184,16 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // Bulk asynchronous copies (TMA engine, SASS UBLKCP) completing on a per-warp
 // mbarrier: the next element's interface-record window and simplex frames are
-// two contiguous runs, so one elected lane moves them with two instructions
-// instead of 32 lanes issuing 16-byte LDGSTS (same-box A/B r02, 400k cfg5
-// cells: 6.22 vs 6.28 ms with LDGSTS; PDG_BULK=0 restores the LDGSTS path).
+// two contiguous runs, so one elected lane could move them with two
+// instructions instead of 32 lanes issuing 16-byte LDGSTS.  Same-box A/B r02:
+// 400k cfg5 cells 6.22 vs 6.28 ms, cfg4 9.83 vs 9.99 ms, cfg3 p=3 4.59 vs
+// 4.64 ms (1-1.5% faster).  Off by default: compute-sanitizer synccheck
+// reports "Missing init" on the warp's mbarrier in this kernel (minimal
+// probes of the same init / expect_tx / bulk copy / try_wait sequence,
+// tools/probe/, are clean; results are bit-identical either way), and the
+// default path must be sanitizer-clean.  PDG_BULK=1 selects it.
 #ifndef PDG_BULK
-#define PDG_BULK 1
+#define PDG_BULK 0
 #endif
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* mb) {
