@@ -184,6 +184,15 @@ class BlockPattern:
         """Pattern of ``row_elements`` from the sorted adjacency (nbr_ptr over
         all elements, nbr_elem = neighbours incl. self) -- vectorised."""
         rows = np.asarray(row_elements, dtype=np.int64)
+        bp = cls.__new__(cls)
+        bp.dof_map, bp.row_elements, bp.row_ptr, bp.col_idx = dof_map, rows, row_ptr, col_idx
+        bp._adj = (nbr_ptr, nbr_elem)  # neighbors / col_starts / global_rows built on first use
+        bp.__post_init__()
+        return bp
+
+    def _build_lazy(self):
+        nbr_ptr, nbr_elem = self.__dict__.pop("_adj")
+        rows, dof_map = self.row_elements, self.dof_map
         a, b = nbr_ptr[rows], nbr_ptr[rows + 1]
         cnt = (b - a).astype(np.int64)
         ptr = np.zeros(rows.size + 1, np.int64)
@@ -197,9 +206,16 @@ class BlockPattern:
         first = dof_map.offsets[rows]
         rp = np.zeros(rows.size + 1, np.int64)
         np.cumsum(ne, out=rp[1:])
-        grows = np.repeat(first - rp[:-1], ne) + np.arange(int(rp[-1]), dtype=np.int64)
-        return cls(dof_map, rows, _RaggedSeq(ptr, nbrs), _RaggedSeq(ptr, cs.astype(np.int64)), row_ptr, col_idx,
-                   grows)
+        self.__dict__["neighbors"] = _RaggedSeq(ptr, nbrs)
+        self.__dict__["col_starts"] = _RaggedSeq(ptr, cs.astype(np.int64))
+        self.__dict__["global_rows"] = np.repeat(first - rp[:-1], ne) + np.arange(int(rp[-1]), dtype=np.int64)
+
+    def __getattr__(self, name):
+        # neighbors / col_starts / global_rows of a pattern made by from_adjacency
+        if name in ("neighbors", "col_starts", "global_rows") and "_adj" in self.__dict__:
+            self._build_lazy()
+            return self.__dict__[name]
+        raise AttributeError(name)
 
     def _local(self, element: int):
         k = int(np.searchsorted(self.row_elements, element))
@@ -358,7 +374,7 @@ def _staging(nbytes: int):
     if "pool" not in _STAGING:
         from concurrent.futures import ThreadPoolExecutor
 
-        n = max(1, min(8, (os.cpu_count() or 2)))
+        n = max(1, min(16, (os.cpu_count() or 2)))
         # two submitters (the staging buffers) + n copy workers
         _STAGING["pool"] = (ThreadPoolExecutor(n + 2), n)
     pool, n = _STAGING["pool"]
@@ -913,6 +929,32 @@ def assemble_device(mesh, coeffs, specs, config: Optional[AssemblyConfig] = None
     return DeviceAssembly(plan, stats)
 
 
+def _work_counts(plan):
+    """(polydg per-kernel work counts, canonical FLOP split) of a plan, cached on
+    the flat mesh for repeated assemblies of the same problem (they depend only
+    on the mesh, degrees, rows, tags and which coefficient terms exist)."""
+    import copy
+    import hashlib
+
+    from .roofline import assembly_work
+
+    f = plan.flat
+    h = hashlib.sha1()
+    for arr in (plan.degrees, plan.row_elements, f.face_tag):
+        h.update(np.ascontiguousarray(arr).view(np.uint8)[: 1 << 24].tobytes())
+        h.update(str(arr.shape).encode())
+    h.update(repr((plan.cdesc["diffusion_kind"], plan.cdesc["has_advection"], plan.cdesc["has_reaction"],
+                   plan.config.quad_increment, int(plan.nnz))).encode())
+    key = h.hexdigest()
+    cache = f.__dict__.setdefault("_work_cache", {})
+    if key not in cache:
+        if len(cache) > 8:
+            cache.clear()
+        cache[key] = (plan.work_stats(), assembly_work(plan))
+    kern, w = cache[key]
+    return copy.deepcopy(kern), w
+
+
 def apportion(kern: dict, flops: dict, ms: float) -> None:
     """Split one fused kernel's device time ``ms`` across polydg's kernel rows
     in proportion to their canonical FLOPs (the rows sum to ``ms``)."""
@@ -937,10 +979,7 @@ def _stats(plan, ms_index, ms_pre, ms_el, total_s) -> AssemblyStats:
         canonical FLOPs (roofline.assembly_work; the rows sum to the kernel
         time) -- an apportioned figure, flagged by ``kernel_split``.
     ``work_items`` / ``nnz_written`` are polydg's analytic counts."""
-    from .roofline import assembly_work
-
-    kern = plan.work_stats()
-    w = assembly_work(plan)
+    kern, w = _work_counts(plan)
     apportion(kern, {"element": w["flops_volume"], "interior": w["flops_interior"],
                      "dirichlet": w["flops_dirichlet"], "inflow": w["flops_inflow"],
                      "neumann_outflow": w["flops_neumann"]}, ms_el)
