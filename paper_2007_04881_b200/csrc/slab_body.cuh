@@ -32,6 +32,21 @@
 
 namespace pdg {
 
+// the slab's values / col_idx are written once and never re-read: streaming
+// (evict-first) stores, as the spatial kernel (PDG_SLAB_ST_CS=0 plain stores)
+#ifndef PDG_SLAB_ST_CS
+#define PDG_SLAB_ST_CS 1
+#endif
+template <class T>
+__device__ __forceinline__ void slab_st(T* p, T v) {
+#if PDG_SLAB_ST_CS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
+
 constexpr int SLAB_KS = 32;       // quadrature slots per round (lane = slot)
 constexpr int SLAB_KSP = 36;      // slot stride (4 mod 16 doubles: conflict-free fragment loads)
 constexpr int SLAB_NBR_MAX = 32;  // neighbours per element staged in shared memory (occupancy: keep small)
@@ -259,7 +274,7 @@ __device__ __forceinline__ void slab_store(double* values, int64_t voff, int64_t
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int r = (wr * TR + i) * 8 + g, cc = (wc * TC + j) * 8 + 2 * t + u;
-        if (r < ne && cc < nj) values[voff + (int64_t)r * L + col0 + cc] = c[i][j][u];
+        if (r < ne && cc < nj) slab_st(values + voff + (int64_t)r * L + col0 + cc, c[i][j][u]);
       }
 }
 
@@ -857,7 +872,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         while (q + 1 < min(nnb, SLAB_NBR_MAX) && nb_col[q + 1] <= p) ++q;
         const int64_t cv = B.dof_offset[nb_j[q]] + (p - nb_col[q]);
         int64_t* dst = a.pat.col_idx + voff + p;
-        for (int r = 0; r < ne; ++r) dst[(int64_t)r * Lrow] = cv;
+        for (int r = 0; r < ne; ++r) slab_st<int64_t>(dst + (int64_t)r * Lrow, cv);
       }
     }
     __syncthreads();
