@@ -374,23 +374,29 @@ def run_ours(args, w, rank, world, local_rank):
         plan.check_flags()
 
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_stop = torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     l0 = lib.pdg_launch_count()
+    # timed: K whole steps back to back (one graph launch per step when
+    # captured); the phase split comes from a separate, untimed event run
     with ClockSampler(local_rank) as clk:
         t_start.record(stream)
         for k in range(K):
-            step(evs[k])
+            step()
         t_stop.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     launches = int(lib.pdg_launch_count() - l0) + (plan.graph_launches * K if graphs else 0)
     ms = t_start.elapsed_time(t_stop) / K
+    KP = min(K, 5)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(KP)]
+    for k in range(KP):
+        step(evs[k])
+    torch.cuda.synchronize(dev)
     ms_index = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     ms_pre = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     ms_el = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)

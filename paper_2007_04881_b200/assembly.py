@@ -744,6 +744,13 @@ class SipgPlan:
                     fn()
                 graphs.append(g)
             self.graph_launches = int(self.lib.pdg_launch_count() - l0)
+            # the whole step as ONE graph (no phase events): one launch per step
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self._index_phase()
+                self._prepass()
+                self._elements()
+            self.graph_step = g
             self.graphs = graphs
             return True
         except Exception as exc:  # capture unsupported: plain launches (same kernels)
@@ -752,8 +759,14 @@ class SipgPlan:
             return False
 
     def run_graphs(self, events=None):
-        """One step through the captured graphs (``capture_graphs``)."""
+        """One step through the captured graphs (``capture_graphs``): the
+        single whole-step graph, or -- with ``events`` (4 CUDA events recorded
+        at the phase boundaries) -- the three per-phase graphs."""
         torch = _torch()
+        if not events and getattr(self, "graph_step", None) is not None:
+            with torch.cuda.stream(self.stream):
+                self.graph_step.replay()
+            return
         with torch.cuda.stream(self.stream):
             for i, g in enumerate(self.graphs):
                 if events:
