@@ -16,6 +16,10 @@ echo "smoke rc=$?"; tail -1 gpurun_out/smoke_${TAG}.log
 fi
 timeout 1200 python bench.py > gpurun_out/bench_cfg5_${TAG}.json 2> gpurun_out/bench_cfg5_${TAG}.err
 echo "bench cfg5 rc=$?"; head -c 600 gpurun_out/bench_cfg5_${TAG}.json; echo
+# the polydg-signature call at the headline scale (100 GB host CSR per call)
+timeout 1200 python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline --e2e-api-max-gb 120 \
+  > gpurun_out/bench_cfg5api_${TAG}.json 2> gpurun_out/bench_cfg5api_${TAG}.err
+echo "bench cfg5 api rc=$? $(python -c "import json; d=json.load(open('gpurun_out/bench_cfg5api_${TAG}.json')); print(d.get('e2e_api'))" 2>&1 | tail -1)"
 for c in cfg1 cfg2 cfg3p2 cfg3p3 cfg3 cfg3p5 cfg3p6 cfg4 st1 st2 st3 st4 st5; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/bench_${c}_${TAG}.json 2> gpurun_out/bench_${c}_${TAG}.err
   echo "bench $c rc=$? $(python -c "import json; d=json.load(open('gpurun_out/bench_${c}_${TAG}.json')); print(round(d['value']/1e6,2), 'M el/s', round(d['ms_per_step'],3), 'ms', round(d['roofline']['frac'],3), 'frac')" 2>&1 | tail -1)"
