@@ -138,19 +138,37 @@ static int jit_rhs_regs_max() {
 // let the register budget, not the CTA granularity, set the resident warp count.
 // Default by dimension (measured r01, same box, cfg4 3D p=2: 4 warps x 3 CTAs
 // 10.25 ms, 2 x 6 9.89 ms, 1 x 12 10.38 ms; 2D keeps 4 x 3).
-static int jit_warps(int dim) {
+// Large bases (p >= 5 in 2D with advection rows) need so much shared memory per
+// warp that 4-warp CTAs leave the SM with a single CTA: the CTA size is then
+// chosen for the most resident warps (<= 12, the 168-register budget), ties
+// going to the measured default (r02, 250k cfg3 p=6 ADR: 4 warps x 1 CTA
+// 48.05 ms, 2 warps x 3 CTAs 44.55 ms; p = 5 and below keep 4-warp CTAs).
+static int jit_warps(int dim, int warp_doubles) {
   const char* v = getenv("PDG_JIT_WARPS");
   const int def = dim == 3 ? 2 : 4;
-  const int w = v ? atoi(v) : def;
-  return w >= 1 && w <= 8 ? w : def;
+  if (v) {
+    const int w = atoi(v);
+    return w >= 1 && w <= 8 ? w : def;
+  }
+  const double budget = 227.0 * 1024 - 4096;  // per SM, minus a rule-table allowance
+  auto resident = [&](int w) {
+    const int ctas = (int)(budget / ((double)w * warp_doubles * 8.0));
+    return std::min(ctas * w, 12);
+  };
+  // switch only for a clear gain (>= 25% more warps): 3D p=2 at 1-warp CTAs
+  // would get 9 instead of 8 warps but measured slower (r01: 10.38 vs 9.89 ms)
+  int best = def, best_r = resident(def);
+  for (int w : {4, 2, 1})
+    if (4 * resident(w) >= 5 * resident(def) && resident(w) > best_r) best = w, best_r = resident(w);
+  return best;
 }
 
-static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv) {
+static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv, int warps) {
   // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow.
   // CTA = 128 threads, default 3 (168 registers, 12 warps/SM;
   //   v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells)
   const char* mb = getenv("PDG_JIT_MINBLOCKS");
-  const int minblocks = mb ? std::max(1, atoi(mb)) : 12 / jit_warps(dim);
+  const int minblocks = mb ? std::max(1, atoi(mb)) : 12 / warps;
   std::ostringstream os;
   os << "#include \"assemble_body.cuh\"\n"
      << "#include \"prepass_body.cuh\"\n"
@@ -161,7 +179,7 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
   if (const char* mr = getenv("PDG_JIT_MAXNREG"))
     os << "__maxnreg__(" << atoi(mr) << ")";
   else
-    os << "__launch_bounds__(" << 32 * jit_warps(dim) << ", " << minblocks << ")";
+    os << "__launch_bounds__(" << 32 * warps << ", " << minblocks << ")";
   os << " pdg_jit_kernel(const __grid_constant__ pdg::KArgs a) {\n"
      << "  pdg::assemble_body<" << dim << ", " << P << ", " << (sym ? "true" : "false")
      << ", pdg_jit::JitCoef, " << kv << ">(a, pdg_jit::JitCoef());\n}\n";
@@ -276,9 +294,10 @@ static std::string get_function(CUmod mod, const char* name, CUfunc& fn) {
   return "";
 }
 
-static std::string get_kernel(const std::string& policy, int dim, int P, bool sym, int kv, JitKernel& out) {
+static std::string get_kernel(const std::string& policy, int dim, int P, bool sym, const AsmLayout& lay,
+                              JitKernel& out) {
   CUmod mod = nullptr;
-  std::string err = get_module(full_source(policy, dim, P, sym, kv), mod);
+  std::string err = get_module(full_source(policy, dim, P, sym, lay.kv, jit_warps(dim, lay.warp_doubles)), mod);
   if (!err.empty()) return err;
   out.mod = mod;
   return get_function(mod, "pdg_jit_kernel", out.fn);
@@ -297,9 +316,9 @@ extern "C" int pdg_jit_prepare(const pdg_coeffs* coeffs, const char* policy_sour
   PDG_TRY {
     if (!coeffs || !policy_source) return fail(PDG_ERR_INVALID, "null argument");
     JitKernel k;
-    const int kv = make_layout(dim, max_degree, coeffs->diffusion_kind,
-                               coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max()).kv;
-    const std::string err = get_kernel(policy_source, dim, max_degree, symmetric_accumulation(*coeffs), kv, k);
+    const AsmLayout lay = make_layout(dim, max_degree, coeffs->diffusion_kind,
+                                      coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max());
+    const std::string err = get_kernel(policy_source, dim, max_degree, symmetric_accumulation(*coeffs), lay, k);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
     return PDG_OK;
   }
@@ -324,9 +343,9 @@ extern "C" int pdg_assemble_jit(const pdg_mesh* mesh, const pdg_basis* basis, co
     KArgs a = make_kargs(mesh, basis, rules, params, *pattern, frames, sigma, face_flow, values, write_col_idx,
                          rhs, err_flags, 0);
     a.lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind, has_vr, jit_rhs_regs_max());
-    const std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, sym, a.lay.kv, k);
+    const std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, sym, a.lay, k);
     if (!err.empty()) return fail(PDG_ERR_UNSUPPORTED, err);
-    int threads = 32 * jit_warps(mesh->dim);
+    int threads = 32 * jit_warps(mesh->dim, a.lay.warp_doubles);
     // the CTA's rule copy (always reserved: the JIT build may toggle PDG_RULES_SMEM)
     size_t smem = ((size_t)rule_smem_doubles(rules->n_points) + (size_t)a.lay.warp_doubles * (threads / 32)) * 8;
     Api& A = api();
@@ -358,10 +377,10 @@ extern "C" int pdg_face_prepass_jit(const pdg_mesh* mesh, const pdg_basis* basis
     const bool iso_var = coeffs->diffusion_kind == PDG_DIFF_ISO && !coeffs->diffusion[0].is_const;
     if (iso_var && !elem_abar) return fail(PDG_ERR_INVALID, "elem_abar scratch required");
     // the module of the element kernel (same policy, dim, degree) carries the pre-pass kernels
-    const int kv = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind,
-                               coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max()).kv;
+    const AsmLayout lay = make_layout(mesh->dim, basis->max_degree, coeffs->diffusion_kind,
+                                      coeffs->has_advection || coeffs->has_reaction, jit_rhs_regs_max());
     JitKernel k;
-    std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, symmetric_accumulation(*coeffs), kv, k);
+    std::string err = get_kernel(policy_source, mesh->dim, basis->max_degree, symmetric_accumulation(*coeffs), lay, k);
     CUfunc fa = nullptr, ff = nullptr;
     if (err.empty()) err = get_function(k.mod, "pdg_jit_abar", fa);
     if (err.empty()) err = get_function(k.mod, "pdg_jit_face_prepass", ff);
