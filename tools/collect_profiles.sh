@@ -2,7 +2,7 @@
 # copy one evidence session's outputs (tools/run_evidence.sh TAG) into profiles/ as <NAME>
 TAG=$1; NAME=${2:-$1}
 set -e
-for f in gpurun_out/bench_*_${TAG}.json gpurun_out/bench2_*_${TAG}.json; do
+for f in gpurun_out/bench_*_${TAG}.json gpurun_out/bench[248]_*_${TAG}.json; do
   b=$(basename $f .json); b=${b%_${TAG}}
   cp $f profiles/${b}_${NAME}.json
 done

@@ -36,6 +36,12 @@ for c in cfg2 cfg4; do
     --master-port 29517 bench.py --gpus 2 --config $c --steps 5 --warmup 3 --no-e2e > gpurun_out/bench2_${c}_${TAG}.json 2> gpurun_out/bench2_${c}_${TAG}.err
   echo "2-rank $c rc=$? $(python -c "import json; d=json.load(open('gpurun_out/bench2_${c}_${TAG}.json')); print(d['scaling'], d['verified'], round(d['ms_per_step'],3))" 2>&1 | tail -1)"
 done
+# the N-rank path with 4 and 8 ranks time-sharing the one GPU (correctness of the split + gather)
+for n in 4 8; do
+  PDG_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+    --master-port 2952$n bench.py --gpus $n --config cfg2 --steps 3 --warmup 3 --no-e2e > gpurun_out/bench${n}_cfg2_${TAG}.json 2> gpurun_out/bench${n}_cfg2_${TAG}.err
+  echo "$n-rank cfg2 rc=$? $(python -c "import json; d=json.load(open('gpurun_out/bench${n}_cfg2_${TAG}.json')); print(d['scaling'], d['verified'], round(d['ms_per_step'],3), d['config']['max_local_elements'])" 2>&1 | tail -1)"
+done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_cfg5_${TAG}.csv python bench.py --steps 2 --warmup 1 --profile \
     > gpurun_out/launches_cfg5_${TAG}.log 2>&1
