@@ -543,6 +543,9 @@ def run_ours(args, w, rank, world, local_rank):
             line["paper_p100_s_per_million_dofs"] = {
                 k: v[w.degree - 1] for k, v in PAPER_P100_S_PER_MDOF.items()}
             line["paper_p100_source"] = "PAPER.md:671-677 (Approach 2, fp64, 1x Tesla P100, not this metric's hardware)"
+    if world > 1 and torch.cuda.device_count() < world:
+        line["note"] = (f"{world} ranks time-share {torch.cuda.device_count()} GPU(s) (PDG_DIST_BACKEND=gloo): "
+                        "a correctness run of the partitioned path, not a scaling measurement")
     if verify is not None:
         line["verified"] = "bitwise" if verify["verified"] else "MISMATCH"
         line["verify_gather"] = {"bytes": verify["bytes"], "seconds": round(verify["seconds"], 2),
