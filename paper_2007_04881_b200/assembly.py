@@ -332,6 +332,12 @@ def download(t, stream=None, chunk_bytes: int = _D2H_CHUNK) -> np.ndarray:
         return out
     stream = stream or torch.cuda.current_stream(t.device)
     per = max(1, chunk_bytes // t.element_size())
+    with _STAGING_LOCK:  # the pinned buffers are process-wide: one download at a time
+        return _download_staged(t, out, n, per, stream)
+
+
+def _download_staged(t, out, n, per, stream):
+    torch = _torch()
     raw, pool, nthreads = _staging(per * t.element_size())
     stages = [r[: per * t.element_size()].view(t.dtype) for r in raw]
     events = [torch.cuda.Event() for _ in range(2)]
@@ -362,6 +368,7 @@ def download(t, stream=None, chunk_bytes: int = _D2H_CHUNK) -> np.ndarray:
 
 
 _STAGING = {}
+_STAGING_LOCK = __import__("threading").Lock()
 
 
 def _staging(nbytes: int):
