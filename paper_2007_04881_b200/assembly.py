@@ -663,19 +663,19 @@ class SipgPlan:
         if size_query:
             self.nnz = int(nnz.value)
 
-    def _frames(self):
+    def _frames(self, stream=None):
         import ctypes as C
 
         _lib.check(self.lib.pdg_frames_build(C.byref(self.dm.struct), C.byref(self.basis),
                                              C.byref(self.frames), _lib.ptr(self.t["flags"]),
-                                             _lib.stream_ptr(self.stream)))
+                                             _lib.stream_ptr(stream or self.stream)))
 
-    def _face_prepass(self):
+    def _face_prepass(self, stream=None):
         import ctypes as C
 
         args = (C.byref(self.rules.struct), C.byref(self.params), _lib.ptr(self.t["sigma"]),
                 _lib.ptr(self.t["flow"]), _lib.ptr(self.t["abar"]), _lib.ptr(self.t["flags"]),
-                _lib.stream_ptr(self.stream))
+                _lib.stream_ptr(stream or self.stream))
         if self.jit_source is not None:  # fields inlined (the NVRTC module of the element kernel)
             _lib.check(self.lib.pdg_face_prepass_jit(C.byref(self.dm.struct), C.byref(self.basis),
                                                      C.byref(self.coeffs), self.jit_source, *args))
@@ -684,10 +684,35 @@ class SipgPlan:
                                                  C.byref(self.coeffs), *args))
 
     def _prepass(self):
-        import ctypes as C
-
         self._frames()
         self._face_prepass()
+        self._records()
+
+    def _index_and_prepass_concurrent(self):
+        """Index phase, frames and the sigma / flow pre-pass are independent:
+        fork them onto three streams (join before the interface records, which
+        read all three).  The whole-step CUDA graph is captured from this, so
+        the small latency-bound kernels overlap instead of queueing."""
+        torch = _torch()
+        if not hasattr(self, "_side"):
+            self._side = [torch.cuda.Stream(self.device) for _ in range(2)]
+            self._ev = [torch.cuda.Event() for _ in range(3)]
+        main = self.stream
+        self._ev[0].record(main)
+        for st in self._side:
+            st.wait_event(self._ev[0])
+        self._frames(stream=self._side[0])
+        self._face_prepass(stream=self._side[1])
+        self._index_phase()
+        self._ev[1].record(self._side[0])
+        self._ev[2].record(self._side[1])
+        main.wait_event(self._ev[1])
+        main.wait_event(self._ev[2])
+        self._records()
+
+    def _records(self):
+        import ctypes as C
+
         _lib.check(self.lib.pdg_iface_records(
             C.byref(self.dm.struct), C.byref(self.basis), C.byref(self.coeffs),
             C.byref(self.rules.struct), C.byref(self.params), C.byref(self.pattern),
@@ -751,11 +776,15 @@ class SipgPlan:
                     fn()
                 graphs.append(g)
             self.graph_launches = int(self.lib.pdg_launch_count() - l0)
-            # the whole step as ONE graph (no phase events): one launch per step
+            # the whole step as ONE graph (no phase events): one launch per step,
+            # index phase / frames / face pre-pass forked onto three streams
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.stream):
-                self._index_phase()
-                self._prepass()
+                if os.environ.get("PDG_FORK", "1") != "0":
+                    self._index_and_prepass_concurrent()
+                else:
+                    self._index_phase()
+                    self._prepass()
                 self._elements()
             self.graph_step = g
             self.graphs = graphs
