@@ -87,8 +87,15 @@ __device__ __forceinline__ void st_out(T* p, T v) {
 
 constexpr int KF = 16;   // face slots per round
 constexpr int KFP = 20;  // face slot stride
-constexpr int NBR_WIN = 16;  // neighbour entries staged per window
-constexpr int FR_MAX = 32;   // simplex frames of one element kept in shared memory
+// neighbour entries staged per window / simplex frames of one element kept in
+// shared memory.  3D uses 12 / 16 (an agglomerated Kuhn element has ~5 tets and
+// ~7 neighbours; the smaller footprint fits 5 instead of 4 two-warp CTAs per SM)
+#ifndef PDG_3D_SMALL
+#define PDG_3D_SMALL 1
+#endif
+__host__ __device__ constexpr int nbr_win(int dim) { return (PDG_3D_SMALL && dim == 3) ? 12 : 16; }
+__host__ __device__ constexpr int fr_max(int dim) { return (PDG_3D_SMALL && dim == 3) ? 16 : 32; }
+constexpr int NBR_WIN_MAX = 16;
 constexpr int REC16 = (int)(sizeof(pdg_iface_rec) / 16);  // 16-byte chunks per interface record
 constexpr int RULE_SMEM_MAX = 128;  // rule tables up to this many points live in shared memory (per CTA)
 #ifndef PDG_RULES_SMEM
@@ -161,14 +168,6 @@ struct Shape {
   static constexpr bool RHS_REGS = NB <= PDG_RHS_REGS_MAX;
 };
 
-// per-warp staging of the neighbour window -- after the scalars
-struct NbrStage {
-  double sig[NBR_WIN];     // penalty of the interface's first face
-  double nrm[3][NBR_WIN];  // its owner normal
-  int j[NBR_WIN], nj[NBR_WIN], col[NBR_WIN], fa[NBR_WIN], fb[NBR_WIN], pj[NBR_WIN];
-  int info[NBR_WIN];       // bit0 e is the neighbour side, bit1 e downwind, bit2 paired-round eligible
-  int row0[NBR_WIN];       // first sub-facet row of the first face
-};
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -307,6 +306,8 @@ template <int DIM, int P, bool SYM, class CF, int KV = 0>
 __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   using S = Shape<DIM, P>;
   using W = Widths<DIM>;
+  constexpr int NBR_WIN = nbr_win(DIM);
+  constexpr int FR_MAX = fr_max(DIM);
   constexpr int NB = S::NB, NT = S::NT, NBP = S::NBP;
   extern __shared__ double smem[];
   const pdg_mesh& m = a.m;

@@ -41,6 +41,7 @@ inline AsmLayout make_layout(int dim, int P, int diff_kind, bool has_vr, int rhs
   if (red > buf) buf = red;
   L.buf_doubles = buf;
   const int W = dim == 2 ? 8 : 16;  // frame record width (Widths<DIM>)
+  const int NBR_WIN = nbr_win(dim), FR_MAX = fr_max(dim);
   L.warp_doubles = buf + 64 + (int)(2 * NBR_WIN * sizeof(pdg_iface_rec) / 8) + (rhs_regs ? 0 : 32 * NB) + FR_MAX * W +
                    (dim == 3 ? 2 : 1) * NBR_WIN * W +  // simplex frames, first facet frames, neighbour basis constants (3D)
                    2;                                  // the warp's mbarrier (8-byte aligned: every term is even)
