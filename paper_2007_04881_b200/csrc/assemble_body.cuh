@@ -50,6 +50,14 @@ namespace pdg {
 // unroll factors of the k-step loops (tuning knobs, PDG_JIT_DEFINES)
 #define PDG_STR_(x) #x
 #define PDG_UNROLL(n) _Pragma(PDG_STR_(unroll n))
+// full unroll of a complete volume round (fixed trip count, compile-time table
+// offsets) vs the PDG_VOL_UNROLL loop (smaller code): -1 = by dimension (2D
+// unrolled; 3D looped -- three gradient rows make the unrolled round big enough
+// to miss in the instruction cache: r02 same-box cfg4 9.59 vs 9.85 ms, while
+// cfg5 / cfg2 lose 1.3% / 2% without it), 0 / 1 force
+#ifndef PDG_VOL_FULL
+#define PDG_VOL_FULL -1
+#endif
 #ifndef PDG_VOL_UNROLL
 #define PDG_VOL_UNROLL 1
 #endif
@@ -621,7 +629,8 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
                 if (!SYM || cc >= r) dmma(cd[r][cc], lf[r], rf[cc]);
           }
         };
-        if (KV && nk == KV / 4) {
+        constexpr bool VOL_FULL = PDG_VOL_FULL < 0 ? DIM == 2 : PDG_VOL_FULL != 0;
+        if (VOL_FULL && KV && nk == KV / 4) {
           // full chunk of a runtime-specialised kernel: fixed trip count and
           // compile-time table offsets
 #pragma unroll
