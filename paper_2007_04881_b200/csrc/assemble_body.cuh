@@ -834,7 +834,10 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         // a single-facet interface takes a paired round, with a partner when
         // the next one qualifies too, else alone (its half of the slots idle;
         // cheaper than the general path: staged frames, one contraction)
-        const bool pair = (rc[qi].info & 4) != 0;
+        // (a 3D face rule of degree >= 1 has >= 9 points: no paired rounds, and
+        // leaving that code out of the 3D kernels keeps them smaller)
+        constexpr bool PAIRS = DIM == 2 || P == 0;
+        const bool pair = PAIRS && (rc[qi].info & 4) != 0;
         const bool has_b = qb < nw && (rc[qb].info & 4);
         double co[NT][NT][2];
         zero_tiles<NT>(co);
