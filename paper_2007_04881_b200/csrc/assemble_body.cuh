@@ -64,6 +64,14 @@ namespace pdg {
 #ifndef PDG_FACE_UNROLL
 #define PDG_FACE_UNROLL 1
 #endif
+// table rows of the padding functions NB <= f < NBP: 0 = not written (they feed
+// only tile rows / columns >= NB, which no store reads; the packed 10-function
+// tile reads function 10 only into columns it discards), 1 = written as zeros,
+// -1 = by dimension (r02 same-box: 2D skips them -- cfg2 1.282 -> 1.255 ms,
+// cfg3 p=3 4.39 -> 4.31, cfg1 18 -> 17 us; 3D writes them -- cfg4 9.52 vs 9.72)
+#ifndef PDG_PAD_ZERO
+#define PDG_PAD_ZERO -1
+#endif
 
 // phase timers (diagnostics: one warp prints its clock64 split at exit)
 #ifndef PDG_TIMERS
@@ -317,6 +325,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   constexpr int NBR_WIN = nbr_win(DIM);
   constexpr int FR_MAX = fr_max(DIM);
   constexpr int NB = S::NB, NT = S::NT, NBP = S::NBP;
+  constexpr int NBW = (PDG_PAD_ZERO < 0 ? DIM == 3 : PDG_PAD_ZERO != 0) ? NBP : NB;  // table functions written per point
   extern __shared__ double smem[];
   const pdg_mesh& m = a.m;
   const pdg_basis& B = a.B;
@@ -490,14 +499,14 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 #pragma unroll
             for (int c = 0; c < DIM; ++c)
 #pragma unroll
-              for (int f = 0; f < NBP; ++f) col[(c * NBP + f) * kvp] = f < NB ? ts.grad(f, c) : 0.0;
+              for (int f = 0; f < NBW; ++f) col[(c * NBP + f) * kvp] = f < NB ? ts.grad(f, c) : 0.0;
           } else if (nG) {
             const double av = dk == PDG_DIFF_ISO ? cf.a_iso(x) : 1.0;
             sc1[lane] = w * av;
 #pragma unroll
             for (int c = 0; c < DIM; ++c)
 #pragma unroll
-              for (int f = 0; f < NBP; ++f) col[(c * NBP + f) * kvp] = f < NB ? tb.grad(f, c) : 0.0;
+              for (int f = 0; f < NBW; ++f) col[(c * NBP + f) * kvp] = f < NB ? tb.grad(f, c) : 0.0;
             if (full) {
               double A[DIM][DIM];
 #pragma unroll
@@ -507,7 +516,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
 #pragma unroll
               for (int c = 0; c < DIM; ++c)
 #pragma unroll
-                for (int f = 0; f < NBP; ++f) {
+                for (int f = 0; f < NBW; ++f) {
                   double v = 0.0;
                   if (f < NB) {
 #pragma unroll
@@ -524,7 +533,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
             for (int i = 0; i < DIM; ++i) bvec[i] = cf.has_adv() ? cf.b_i(i, x) : 0.0;
             const double cr = cf.has_reac() ? cf.c(x) : 0.0;
 #pragma unroll
-            for (int f = 0; f < NBP; ++f) {
+            for (int f = 0; f < NBW; ++f) {
               double vv = 0.0, rr = 0.0;
               if (f < NB) {
                 vv = tb.val(f);
@@ -701,7 +710,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           yc[k] = nrm[1] * tb.d1[1][k];
         }
 #pragma unroll
-        for (int ff = 0; ff < NBP; ++ff) {
+        for (int ff = 0; ff < NBW; ++ff) {
           double vv = 0.0, fl = 0.0;
           if (ff < NB) {
             const int ia = mi.a[ff][0], ib = mi.a[ff][1];
@@ -716,7 +725,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         }
       } else {
 #pragma unroll
-        for (int ff = 0; ff < NBP; ++ff) {
+        for (int ff = 0; ff < NBW; ++ff) {
           double vv = 0.0, fl = 0.0;
           if (ff < NB) {
             vv = tb.val(ff);
@@ -986,7 +995,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           }
           double* col = buf + slot;
 #pragma unroll
-          for (int ff = 0; ff < NBP; ++ff) {
+          for (int ff = 0; ff < NBW; ++ff) {
             double vv = 0.0, fl = 0.0;
             if (ff < NB) {
               vv = tb.val(ff);
