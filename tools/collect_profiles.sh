@@ -17,4 +17,5 @@ cp gpurun_out/box_${TAG}.txt profiles/box_${NAME}.txt 2>/dev/null || true
 for t in memcheck racecheck synccheck initcheck; do
   [ -f gpurun_out/sanitizer_${t}_${TAG}.log ] && grep -vE "^=========     (Host Frame|Saved host)" gpurun_out/sanitizer_${t}_${TAG}.log | head -400 > profiles/sanitizer_${t}_${NAME}.log
 done
+python tools/traffic_json.py ${NAME}
 echo collected
