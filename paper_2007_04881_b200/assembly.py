@@ -895,14 +895,20 @@ class SipgPlan:
 
 
 class HostIO:
-    """Pinned-host staging for end-to-end runs of a plan: every ``upload()``
-    copies the mesh arrays host->device (the assembly inputs), every
-    ``download()`` moves the assembled CSR (row_ptr, col_idx, values) and the
-    RHS device->host through a pinned staging ring of ``chunk_bytes``.  The
-    bytes moved are the full result; only the host-side retention is bounded
-    (a 4M-element p=4 matrix is ~100 GB)."""
+    """Host buffers for end-to-end runs of a plan (a caller that keeps its
+    result arrays across assemblies).
 
-    def __init__(self, plan: "SipgPlan", chunk_bytes: int = 1 << 30):
+    Every ``upload()`` copies the mesh arrays host->device (the assembly
+    inputs).  Every ``download()`` moves the assembled CSR (row_ptr, col_idx,
+    values) and the RHS device->host.  With ``retain`` (default) they land in
+    host arrays registered with the driver (page-locked, so the copies are
+    DMA at the link rate), and ``result()`` returns them as a host
+    ``CSRMatrix`` + RHS.  When registration fails (locked-memory limit), or
+    with ``retain=False``, the bytes go through a pinned ring of
+    ``chunk_bytes`` and nothing is retained (``retained`` says which).
+    ``close()`` unregisters and releases the host arrays."""
+
+    def __init__(self, plan: "SipgPlan", chunk_bytes: int = 1 << 30, retain: bool = True):
         torch = _torch()
         self.plan = plan
         self.inputs = {}
@@ -912,9 +918,21 @@ class HostIO:
             h.copy_(src)
             self.inputs[attr] = h
         self.h2d_bytes = sum(int(t.numel() * t.element_size()) for t in self.inputs.values())
-        self.stage = torch.empty(chunk_bytes, dtype=torch.uint8, pin_memory=True)
         outs = (plan.row_ptr, plan.col_idx, plan.values, plan.rhs)
         self.d2h_bytes = sum(int(t.numel() * t.element_size()) for t in outs)
+        self.host, self.stage = [], None
+        if retain:
+            try:
+                for t in outs:
+                    self.host.append(_registered_empty(t))
+            except RuntimeError:
+                self.close()
+        if not self.host:
+            self.stage = torch.empty(chunk_bytes, dtype=torch.uint8, pin_memory=True)
+
+    @property
+    def retained(self) -> bool:
+        return bool(self.host)
 
     def upload(self):
         torch = _torch()
@@ -925,13 +943,44 @@ class HostIO:
     def download(self):
         torch = _torch()
         p = self.plan
-        cap = self.stage.numel()
+        outs = (p.row_ptr, p.col_idx, p.values, p.rhs)
         with torch.cuda.stream(p.stream):
-            for t in (p.row_ptr, p.col_idx, p.values, p.rhs):
+            if self.host:
+                for t, (_, h) in zip(outs, self.host):
+                    h.copy_(t.reshape(-1), non_blocking=True)
+                return
+            cap = self.stage.numel()
+            for t in outs:
                 flat = t.reshape(-1).view(torch.uint8)
                 for a in range(0, flat.numel(), cap):
                     b = min(a + cap, flat.numel())
                     self.stage[: b - a].copy_(flat[a:b], non_blocking=True)
+
+    def result(self):
+        """(CSRMatrix, rhs) of the last download (after the stream is synchronised)."""
+        if not self.host:
+            raise AssemblyError("HostIO(retain=False) keeps no host copy")
+        (rp, _), (ci, _), (va, _), (rh, _) = self.host
+        return CSRMatrix(self.plan.n_local_rows, self.plan.dof.n_dofs, rp, ci, va), rh
+
+    def close(self):
+        torch = _torch()
+        for arr, _ in self.host:
+            if arr.nbytes:
+                torch._C._cudart.cudaHostUnregister(arr.ctypes.data)
+        self.host = []
+
+
+def _registered_empty(t):
+    """Host numpy array shaped like device tensor ``t`` (flattened), page-locked
+    with cudaHostRegister, and a torch view of it (so copies are async DMA)."""
+    torch = _torch()
+    arr = np.empty(int(t.numel()), dtype=np.dtype(str(t.dtype).replace("torch.", "")))
+    if arr.nbytes:
+        rc = torch._C._cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+        if int(rc) != 0:
+            raise RuntimeError(f"cudaHostRegister failed ({rc})")
+    return arr, torch.from_numpy(arr)
 
 
 @dataclass

@@ -314,3 +314,37 @@ def test_pinned_chunked_download_and_block_slots_on_assembled_matrix():
         for j in pattern.neighbors[k]:
             sl = pattern.block_slots(int(e), int(j))
             assert np.array_equal(m.values[sl], dense[off[e]:off[e + 1], off[j]:off[j + 1]])
+
+
+def test_hostio_retained_host_csr_matches_assembly():
+    """HostIO (the bench's e2e leg): uploads the mesh, downloads into
+    registered host arrays, and result() is the assembled CSR + RHS; after
+    close() the arrays are released (result raises)."""
+    import torch
+
+    from paper_2007_04881_b200.assembly import AssemblyError, HostIO, SipgPlan
+
+    pm = _mesh("clusters10")
+    coeffs = F.generic(2)
+    classify_boundary_faces(pm, coeffs)
+    specs = build_basis(pm, 3)
+    m, rhs, _, _ = assemble_approach2(pm, coeffs, specs)
+    plan = SipgPlan(pm, coeffs, specs)
+    io = HostIO(plan)
+    assert io.retained
+    for _ in range(2):
+        io.upload()
+        plan.run()
+        io.download()
+    torch.cuda.synchronize()
+    mh, rh = io.result()
+    assert mh.n_rows == m.n_rows and mh.n_cols == m.n_cols
+    assert np.array_equal(mh.row_ptr, m.row_ptr) and np.array_equal(mh.col_idx, m.col_idx)
+    assert np.array_equal(mh.values, m.values) and np.array_equal(rh, rhs)
+    io.close()
+    with pytest.raises(AssemblyError):
+        io.result()
+    ring = HostIO(plan, retain=False)
+    assert not ring.retained
+    ring.upload(); plan.run(); ring.download()
+    torch.cuda.synchronize()
