@@ -433,12 +433,12 @@ def run_ours(args, w, rank, world, local_rank):
                 and np.array_equal(rhs_hh, plan.rhs.cpu().numpy())
                 and np.array_equal(mat_h.values[::st], plan.values[::st].cpu().numpy())
                 and np.array_equal(mat_h.col_idx[::st], plan.col_idx[::st].cpu().numpy()))
-            e2e_host["how"] = ("D2H into host CSR arrays registered with cudaHostRegister (page-locked, kept "
-                               "across steps, HostIO.result()); checked against the device CSR after the "
+            e2e_host["how"] = ("D2H into page-locked host CSR arrays (pdg_host_alloc, kept across steps, "
+                               "HostIO.result()); checked against the device CSR after the "
                                f"timed region (row_ptr, rhs whole; values, col_idx every {st}th entry)")
             del mat_h, rhs_hh
         else:
-            e2e_host["how"] = "D2H through a 1 GiB pinned ring (host registration failed)"
+            e2e_host["how"] = "D2H through a 1 GiB pinned ring (page-locked host allocation failed)"
         io.close()
         del io
 

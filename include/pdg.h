@@ -253,6 +253,12 @@ const char* pdg_last_error(void);
  * accounting: the driver compares it with the profiler's launch list). */
 int64_t pdg_launch_count(void);
 
+/* Page-locked host memory for result buffers a caller keeps across
+ * assemblies (device->host copies at the link's DMA rate; the host side of
+ * polydg's returned CSRMatrix, assembly.py:1117-1134).  *out = NULL for 0 bytes. */
+int pdg_host_alloc(size_t bytes, void** out);
+int pdg_host_free(void* p);
+
 /* Bytes of device scratch needed by pdg_adjacency / pdg_pattern_offsets. */
 size_t pdg_workspace_bytes(int64_t n_elements, int64_t n_interfaces);
 

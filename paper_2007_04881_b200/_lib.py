@@ -126,7 +126,8 @@ EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspa
            "pdg_a1_emit", "pdg_triplets_workspace_bytes", "pdg_triplets_to_csr", "pdg_triplets_to_vector",
            "pdg_agglomerate_workspace_bytes", "pdg_agglomerate",
            "pdg_spmv_blocked", "pdg_block_jacobi_setup", "pdg_block_jacobi_apply",
-           "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks", "pdg_face_blocks", "pdg_eval_coeffs")
+           "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks", "pdg_face_blocks", "pdg_eval_coeffs",
+           "pdg_host_alloc", "pdg_host_free")
 
 
 class EngineUnavailable(RuntimeError):
@@ -186,6 +187,8 @@ def load():
     lib.pdg_face_blocks.argtypes = [P(Mesh), P(Basis), P(Coeffs), P(Rules), P(Params), _p, _i64, _p, _p,
                                     _p, _p]
     lib.pdg_eval_coeffs.argtypes = [_i32, P(Coeffs), _p, _i64, _p, _p]
+    lib.pdg_host_alloc.argtypes = [C.c_size_t, P(C.c_void_p)]
+    lib.pdg_host_free.argtypes = [C.c_void_p]
     for name in EXPORTS:
         if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes",
                         "pdg_triplets_workspace_bytes", "pdg_agglomerate_workspace_bytes"):

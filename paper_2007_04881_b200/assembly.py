@@ -901,12 +901,12 @@ class HostIO:
     Every ``upload()`` copies the mesh arrays host->device (the assembly
     inputs).  Every ``download()`` moves the assembled CSR (row_ptr, col_idx,
     values) and the RHS device->host.  With ``retain`` (default) they land in
-    host arrays registered with the driver (page-locked, so the copies are
-    DMA at the link rate), and ``result()`` returns them as a host
-    ``CSRMatrix`` + RHS.  When registration fails (locked-memory limit), or
-    with ``retain=False``, the bytes go through a pinned ring of
-    ``chunk_bytes`` and nothing is retained (``retained`` says which).
-    ``close()`` unregisters and releases the host arrays."""
+    page-locked host arrays (``pdg_host_alloc``: the copies are DMA at the
+    link rate -- on the box 51 GB/s, against 47 GB/s into registered pageable
+    arrays, tools/register_probe.py), and ``result()`` returns them as a host
+    ``CSRMatrix`` + RHS.  When the allocation fails, or with
+    ``retain=False``, the bytes go through a pinned ring of ``chunk_bytes``
+    and nothing is retained (``retained`` says which)."""
 
     def __init__(self, plan: "SipgPlan", chunk_bytes: int = 1 << 30, retain: bool = True):
         torch = _torch()
@@ -924,8 +924,8 @@ class HostIO:
         if retain:
             try:
                 for t in outs:
-                    self.host.append(_registered_empty(t))
-            except RuntimeError:
+                    self.host.append(_pinned_empty(t))
+            except RuntimeError:  # out of page-lockable memory: fall back to the ring
                 self.close()
         if not self.host:
             self.stage = torch.empty(chunk_bytes, dtype=torch.uint8, pin_memory=True)
@@ -946,7 +946,7 @@ class HostIO:
         outs = (p.row_ptr, p.col_idx, p.values, p.rhs)
         with torch.cuda.stream(p.stream):
             if self.host:
-                for t, (_, h) in zip(outs, self.host):
+                for t, (_, h, _) in zip(outs, self.host):
                     h.copy_(t.reshape(-1), non_blocking=True)
                 return
             cap = self.stage.numel()
@@ -957,30 +957,50 @@ class HostIO:
                     self.stage[: b - a].copy_(flat[a:b], non_blocking=True)
 
     def result(self):
-        """(CSRMatrix, rhs) of the last download (after the stream is synchronised)."""
+        """(CSRMatrix, rhs) of the last download (after the stream is
+        synchronised): views of the page-locked buffers, overwritten by the
+        next ``download()``."""
         if not self.host:
             raise AssemblyError("HostIO(retain=False) keeps no host copy")
-        (rp, _), (ci, _), (va, _), (rh, _) = self.host
+        (rp, _, _), (ci, _, _), (va, _, _), (rh, _, _) = self.host
         return CSRMatrix(self.plan.n_local_rows, self.plan.dof.n_dofs, rp, ci, va), rh
 
     def close(self):
-        torch = _torch()
-        for arr, _ in self.host:
-            if arr.nbytes:
-                torch._C._cudart.cudaHostUnregister(arr.ctypes.data)
+        """Drop the host arrays: their page-locked memory is freed when the
+        last view of it (e.g. a ``result()`` array the caller kept) is gone."""
         self.host = []
 
 
-def _registered_empty(t):
-    """Host numpy array shaped like device tensor ``t`` (flattened), page-locked
-    with cudaHostRegister, and a torch view of it (so copies are async DMA)."""
+class _PinnedBlock:
+    """Owner of one pdg_host_alloc block (freed with the last numpy view)."""
+
+    def __init__(self, ptr: int):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            _lib.load().pdg_host_free(self.ptr)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def _pinned_empty(t):
+    """Page-locked host array shaped like device tensor ``t`` (flattened), a
+    torch view of it (copies into it are async DMA) and its pointer."""
+    import ctypes as C
+
     torch = _torch()
-    arr = np.empty(int(t.numel()), dtype=np.dtype(str(t.dtype).replace("torch.", "")))
-    if arr.nbytes:
-        rc = torch._C._cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
-        if int(rc) != 0:
-            raise RuntimeError(f"cudaHostRegister failed ({rc})")
-    return arr, torch.from_numpy(arr)
+    dt = np.dtype(str(t.dtype).replace("torch.", ""))
+    n = int(t.numel())
+    ptr = C.c_void_p()
+    _lib.check(_lib.load().pdg_host_alloc(n * dt.itemsize, C.byref(ptr)))
+    if not ptr.value:
+        arr = np.empty(n, dt)
+    else:
+        buf = (C.c_char * (n * dt.itemsize)).from_address(ptr.value)
+        buf._owner = _PinnedBlock(ptr.value)  # numpy views keep buf, buf keeps the block
+        arr = np.frombuffer(buf, dtype=dt, count=n)
+    return arr, torch.from_numpy(arr), ptr.value
 
 
 @dataclass

@@ -145,6 +145,25 @@ extern "C" int64_t pdg_launch_count(void) { return (int64_t)g_launches.load(); }
 
 extern "C" const char* pdg_last_error(void) { return g_last_error.c_str(); }
 
+extern "C" int pdg_host_alloc(size_t bytes, void** out) {
+  PDG_TRY {
+    if (!out) return fail(PDG_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (bytes == 0) return PDG_OK;
+    PDG_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
+extern "C" int pdg_host_free(void* p) {
+  PDG_TRY {
+    if (p) PDG_CUDA(cudaFreeHost(p));
+    return PDG_OK;
+  }
+  PDG_CATCH
+}
+
 extern "C" int pdg_assemble(const pdg_mesh* mesh, const pdg_basis* basis, const pdg_coeffs* coeffs,
                             const pdg_rules* rules, const pdg_params* params, const pdg_pattern* pattern,
                             const pdg_frames* frames, const double* sigma, const int8_t* face_flow,

@@ -318,8 +318,8 @@ def test_pinned_chunked_download_and_block_slots_on_assembled_matrix():
 
 def test_hostio_retained_host_csr_matches_assembly():
     """HostIO (the bench's e2e leg): uploads the mesh, downloads into
-    registered host arrays, and result() is the assembled CSR + RHS; after
-    close() the arrays are released (result raises)."""
+    page-locked host arrays, and result() is the assembled CSR + RHS; close()
+    drops them (result raises; arrays the caller kept stay valid)."""
     import torch
 
     from paper_2007_04881_b200.assembly import AssemblyError, HostIO, SipgPlan
@@ -344,6 +344,9 @@ def test_hostio_retained_host_csr_matches_assembly():
     io.close()
     with pytest.raises(AssemblyError):
         io.result()
+    # the page-locked memory lives as long as a view of it
+    assert np.array_equal(mh.values, m.values) and np.array_equal(rh, rhs)
+    del mh, rh
     ring = HostIO(plan, retain=False)
     assert not ring.retained
     ring.upload(); plan.run(); ring.download()
