@@ -143,6 +143,12 @@ static int jit_rhs_regs_max() {
 // chosen for the most resident warps (<= 12, the 168-register budget), ties
 // going to the measured default (r02, 250k cfg3 p=6 ADR: 4 warps x 1 CTA
 // 48.05 ms, 2 warps x 3 CTAs 44.55 ms; p = 5 and below keep 4-warp CTAs).
+// CTAs of w warps that fit one SM's shared memory
+static int smem_ctas(int w, int warp_doubles) {
+  const double budget = 227.0 * 1024 - 4096;  // per SM, minus a rule-table allowance
+  return (int)(budget / ((double)w * warp_doubles * 8.0));
+}
+
 static int jit_warps(int dim, int warp_doubles) {
   const char* v = getenv("PDG_JIT_WARPS");
   const int def = dim == 3 ? 2 : 4;
@@ -150,11 +156,7 @@ static int jit_warps(int dim, int warp_doubles) {
     const int w = atoi(v);
     return w >= 1 && w <= 8 ? w : def;
   }
-  const double budget = 227.0 * 1024 - 4096;  // per SM, minus a rule-table allowance
-  auto resident = [&](int w) {
-    const int ctas = (int)(budget / ((double)w * warp_doubles * 8.0));
-    return std::min(ctas * w, 12);
-  };
+  auto resident = [&](int w) { return std::min(smem_ctas(w, warp_doubles) * w, 12); };
   // switch only for a clear gain (>= 25% more warps): 3D p=2 at 1-warp CTAs
   // would get 9 instead of 8 warps but measured slower (r01: 10.38 vs 9.89 ms)
   int best = def, best_r = resident(def);
@@ -163,12 +165,19 @@ static int jit_warps(int dim, int warp_doubles) {
   return best;
 }
 
-static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv, int warps) {
+static std::string full_source(const std::string& policy, int dim, int P, bool sym, int kv, int warps,
+                               int warp_doubles) {
   // PDG_JIT_MINBLOCKS: minimum resident CTAs per SM the compiler must allow.
-  // CTA = 128 threads, default 3 (168 registers, 12 warps/SM;
-  //   v2 measured 2/3/4 -> 11.0/9.2/8.95 ms, v3 3/4 -> 7.47/7.75 ms, 400k cfg5 cells)
+  // Default: 12 warps per SM (168 registers; 4-warp CTAs x 3) when shared
+  // memory fits them (v2 measured 2/3/4 CTAs -> 11.0/9.2/8.95 ms, v3 3/4 ->
+  // 7.47/7.75 ms, 400k cfg5 cells).  When shared memory already holds the SM
+  // below 12 warps, no bound: ptxas may use up to 255 registers (r02 same box:
+  // cfg3 p=4 / 5 / 6 ADR 6.71 -> 6.01, 17.06 -> 15.41, 45.0 -> 34.5 ms; cfg4 3D
+  // 9.53 -> 9.11 ms at 8 instead of 10 warps; register-limited kernels lose:
+  // cfg5 6.26 -> 7.30, cfg2 1.25 -> 1.47 ms).
   const char* mb = getenv("PDG_JIT_MINBLOCKS");
-  const int minblocks = mb ? std::max(1, atoi(mb)) : 12 / warps;
+  const bool smem_bound = smem_ctas(warps, warp_doubles) * warps < 12;
+  const int minblocks = (mb && *mb) ? std::max(1, atoi(mb)) : (smem_bound ? 1 : 12 / warps);
   std::ostringstream os;
   os << "#include \"assemble_body.cuh\"\n"
      << "#include \"prepass_body.cuh\"\n"
@@ -297,7 +306,7 @@ static std::string get_function(CUmod mod, const char* name, CUfunc& fn) {
 static std::string get_kernel(const std::string& policy, int dim, int P, bool sym, const AsmLayout& lay,
                               JitKernel& out) {
   CUmod mod = nullptr;
-  std::string err = get_module(full_source(policy, dim, P, sym, lay.kv, jit_warps(dim, lay.warp_doubles)), mod);
+  std::string err = get_module(full_source(policy, dim, P, sym, lay.kv, jit_warps(dim, lay.warp_doubles), lay.warp_doubles), mod);
   if (!err.empty()) return err;
   out.mod = mod;
   return get_function(mod, "pdg_jit_kernel", out.fn);
