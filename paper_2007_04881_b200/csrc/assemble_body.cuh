@@ -50,11 +50,19 @@ namespace pdg {
 // unroll factors of the k-step loops (tuning knobs, PDG_JIT_DEFINES)
 #define PDG_STR_(x) #x
 #define PDG_UNROLL(n) _Pragma(PDG_STR_(unroll n))
+// PDG_REG_CAPPED: 1 when the kernel is compiled for 12 warps/SM (168
+// registers), 0 when shared memory already limits residency and ptxas may use
+// up to 255 registers (pdg_jit.cu full_source sets it).  Two 3D defaults below
+// depend on it.
+#ifndef PDG_REG_CAPPED
+#define PDG_REG_CAPPED 1
+#endif
 // full unroll of a complete volume round (fixed trip count, compile-time table
-// offsets) vs the PDG_VOL_UNROLL loop (smaller code): -1 = by dimension (2D
-// unrolled; 3D looped -- three gradient rows make the unrolled round big enough
-// to miss in the instruction cache: r02 same-box cfg4 9.59 vs 9.85 ms, while
-// cfg5 / cfg2 lose 1.3% / 2% without it), 0 / 1 force
+// offsets) vs the PDG_VOL_UNROLL loop (smaller code): -1 = 2D unrolled; 3D
+// looped when register-capped -- three gradient rows make the unrolled round
+// big enough to miss in the instruction cache: r02 same-box cfg4 9.59 vs 9.85
+// ms, while cfg5 / cfg2 lose 1.3% / 2% without it -- and unrolled with 255
+// registers (cfg4 8.80 vs 9.10 ms together with PDG_PAD_ZERO), 0 / 1 force
 #ifndef PDG_VOL_FULL
 #define PDG_VOL_FULL -1
 #endif
@@ -67,8 +75,9 @@ namespace pdg {
 // table rows of the padding functions NB <= f < NBP: 0 = not written (they feed
 // only tile rows / columns >= NB, which no store reads; the packed 10-function
 // tile reads function 10 only into columns it discards), 1 = written as zeros,
-// -1 = by dimension (r02 same-box: 2D skips them -- cfg2 1.282 -> 1.255 ms,
-// cfg3 p=3 4.39 -> 4.31, cfg1 18 -> 17 us; 3D writes them -- cfg4 9.52 vs 9.72)
+// -1 = skipped except in register-capped 3D kernels (r02 same-box: 2D --
+// cfg2 1.282 -> 1.255 ms, cfg3 p=3 4.39 -> 4.31, cfg1 18 -> 17 us; 3D at 168
+// registers writes them -- cfg4 9.52 vs 9.72 -- at 255 skips them)
 #ifndef PDG_PAD_ZERO
 #define PDG_PAD_ZERO -1
 #endif
@@ -325,7 +334,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
   constexpr int NBR_WIN = nbr_win(DIM);
   constexpr int FR_MAX = fr_max(DIM);
   constexpr int NB = S::NB, NT = S::NT, NBP = S::NBP;
-  constexpr int NBW = (PDG_PAD_ZERO < 0 ? DIM == 3 : PDG_PAD_ZERO != 0) ? NBP : NB;  // table functions written per point
+  constexpr int NBW = (PDG_PAD_ZERO < 0 ? (DIM == 3 && PDG_REG_CAPPED) : PDG_PAD_ZERO != 0) ? NBP : NB;  // table functions written per point
   extern __shared__ double smem[];
   const pdg_mesh& m = a.m;
   const pdg_basis& B = a.B;
@@ -638,7 +647,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
                 if (!SYM || cc >= r) dmma(cd[r][cc], lf[r], rf[cc]);
           }
         };
-        constexpr bool VOL_FULL = PDG_VOL_FULL < 0 ? DIM == 2 : PDG_VOL_FULL != 0;
+        constexpr bool VOL_FULL = PDG_VOL_FULL < 0 ? (DIM == 2 || !PDG_REG_CAPPED) : PDG_VOL_FULL != 0;
         if (VOL_FULL && KV && nk == KV / 4) {
           // full chunk of a runtime-specialised kernel: fixed trip count and
           // compile-time table offsets
