@@ -151,7 +151,10 @@ static int smem_ctas(int w, int warp_doubles) {
 
 static int jit_warps(int dim, int warp_doubles) {
   const char* v = getenv("PDG_JIT_WARPS");
-  const int def = dim == 3 ? 2 : 4;
+  // 3D kernels that shared memory holds below 12 warps compile with up to 255
+  // registers (full_source): 1-warp CTAs then measured best (r02, cfg4 8.66 vs
+  // 8.79 ms at 2 warps, 9.03 at 4)
+  const int def = dim == 3 ? (smem_ctas(2, warp_doubles) * 2 < 12 ? 1 : 2) : 4;
   if (v) {
     const int w = atoi(v);
     return w >= 1 && w <= 8 ? w : def;
