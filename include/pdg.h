@@ -259,6 +259,17 @@ int64_t pdg_launch_count(void);
 int pdg_host_alloc(size_t bytes, void** out);
 int pdg_host_free(void* p);
 
+/* col_idx crosses the link once per element: every row of an element's block
+ * row has the same columns (assembly.py:316-324).  pdg_pack_block_cols gathers
+ * each element's first row, packed[pack_offset[k] ..] (pack_offset = exclusive
+ * scan of row_len, device arrays); pdg_expand_block_cols writes it back into
+ * every row of a host col_idx (host arrays: elem_row_offset [n+1] local first
+ * rows, row_ptr, packed; n_threads host threads). */
+int pdg_pack_block_cols(const int64_t* col_idx, const int64_t* elem_val_offset, const int64_t* row_len,
+                        const int64_t* pack_offset, int64_t n_row_elements, int64_t* packed, pdg_stream stream);
+int pdg_expand_block_cols(int64_t n_row_elements, const int64_t* elem_row_offset, const int64_t* row_ptr,
+                          const int64_t* packed, int64_t* col_idx, int32_t n_threads);
+
 /* Bytes of device scratch needed by pdg_adjacency / pdg_pattern_offsets. */
 size_t pdg_workspace_bytes(int64_t n_elements, int64_t n_interfaces);
 

@@ -127,7 +127,7 @@ EXPORTS = ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspa
            "pdg_agglomerate_workspace_bytes", "pdg_agglomerate",
            "pdg_spmv_blocked", "pdg_block_jacobi_setup", "pdg_block_jacobi_apply",
            "pdg_map_simplices", "pdg_tabulate", "pdg_element_blocks", "pdg_face_blocks", "pdg_eval_coeffs",
-           "pdg_host_alloc", "pdg_host_free")
+           "pdg_host_alloc", "pdg_host_free", "pdg_pack_block_cols", "pdg_expand_block_cols")
 
 
 class EngineUnavailable(RuntimeError):
@@ -189,6 +189,8 @@ def load():
     lib.pdg_eval_coeffs.argtypes = [_i32, P(Coeffs), _p, _i64, _p, _p]
     lib.pdg_host_alloc.argtypes = [C.c_size_t, P(C.c_void_p)]
     lib.pdg_host_free.argtypes = [C.c_void_p]
+    lib.pdg_pack_block_cols.argtypes = [_p, _p, _p, _p, _i64, _p, _p]
+    lib.pdg_expand_block_cols.argtypes = [_i64, _p, _p, _p, _p, _i32]
     for name in EXPORTS:
         if name not in ("pdg_abi_version", "pdg_last_error", "pdg_launch_count", "pdg_workspace_bytes",
                         "pdg_triplets_workspace_bytes", "pdg_agglomerate_workspace_bytes"):

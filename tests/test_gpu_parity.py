@@ -347,6 +347,14 @@ def test_hostio_retained_host_csr_matches_assembly():
     # the page-locked memory lives as long as a view of it
     assert np.array_equal(mh.values, m.values) and np.array_equal(rh, rhs)
     del mh, rh
+    full = HostIO(plan, compact_cols=False)  # every row of col_idx over the link
+    full.upload(); plan.run(); full.download()
+    torch.cuda.synchronize()
+    mf, rf = full.result()
+    assert np.array_equal(mf.col_idx, m.col_idx) and np.array_equal(mf.values, m.values)
+    assert full.d2h_bytes > io.d2h_bytes
+    del mf, rf
+    full.close()
     ring = HostIO(plan, retain=False)
     assert not ring.retained
     ring.upload(); plan.run(); ring.download()

@@ -55,6 +55,30 @@ def test_library_rejects_bad_arguments_without_a_gpu():
                             None, 0, None, None, None) == _lib.PDG_ERR_UNSUPPORTED
 
 
+def test_expand_block_cols_rebuilds_every_row_on_the_host():
+    """pdg_expand_block_cols (host threads, no GPU): one packed column list per
+    element -> the same list in each of the element's rows, for ragged row
+    counts / lengths, empty lists and any thread count (HostIO's e2e path)."""
+    rng = np.random.default_rng(3)
+    n = 257
+    ne = rng.integers(1, 7, n)
+    L = rng.integers(0, 40, n)
+    L[5] = 0
+    row0 = np.concatenate([[0], np.cumsum(ne)]).astype(np.int64)
+    row_len = np.repeat(L, ne)
+    row_ptr = np.concatenate([[0], np.cumsum(row_len)]).astype(np.int64)
+    lists = [np.sort(rng.choice(10_000, int(l), replace=False)).astype(np.int64) for l in L]
+    packed = np.concatenate(lists).astype(np.int64)
+    want = np.concatenate([np.tile(c, int(k)) for c, k in zip(lists, ne)]).astype(np.int64)
+    lib = _lib.load()
+    for nt in (1, 3, 16):
+        out = np.full(row_ptr[-1], -1, np.int64)
+        _lib.check(lib.pdg_expand_block_cols(n, row0.ctypes.data, row_ptr.ctypes.data, packed.ctypes.data,
+                                             out.ctypes.data, nt))
+        assert np.array_equal(out, want)
+    assert lib.pdg_expand_block_cols(n, None, None, None, None, 1) == _lib.PDG_ERR_INVALID
+
+
 # ---- meshes ------------------------------------------------------------------------
 
 def _flat_equal(a: FlatMesh, b: FlatMesh):
