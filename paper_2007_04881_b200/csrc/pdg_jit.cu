@@ -182,7 +182,7 @@ static std::string full_source(const std::string& policy, int dim, int P, bool s
   const bool smem_bound = smem_ctas(warps, warp_doubles) * warps < 12;
   const int minblocks = (mb && *mb) ? std::max(1, atoi(mb)) : (smem_bound ? 1 : 12 / warps);
   std::ostringstream os;
-  os << "#define PDG_REG_CAPPED " << (minblocks * warps >= 12 ? 1 : 0) << "\n"
+  os << "#ifndef PDG_REG_CAPPED\n#define PDG_REG_CAPPED " << (minblocks * warps >= 12 ? 1 : 0) << "\n#endif\n"
      << "#include \"assemble_body.cuh\"\n"
      << "#include \"prepass_body.cuh\"\n"
      << "namespace pdg_jit {\nusing namespace pdg;\n"

@@ -129,11 +129,16 @@ def test_sign_changing_diffusion_reruns_plain_volume():
 
 
 @pytest.mark.parametrize("env", [{"PDG_JIT": "0"}, {"PDG_PLAIN_VOLUME": "1"},
-                                 {"PDG_JIT": "0", "PDG_PLAIN_VOLUME": "1"}])
+                                 {"PDG_JIT": "0", "PDG_PLAIN_VOLUME": "1"},
+                                 {"PDG_JIT_DEFINES": "-DPDG_BULK=1"},
+                                 {"PDG_JIT_MINBLOCKS": "1"},
+                                 {"PDG_JIT_DEFINES": "-DPDG_PAD_ZERO=1 -DPDG_VOL_FULL=0 -DPDG_REG_CAPPED=0"}])
 @pytest.mark.parametrize("case", ["vardiff", "adr", "aniso3d"])
 def test_kernel_variants(monkeypatch, env, case):
-    """The ahead-of-time (bytecode-interpreted) kernels and the plain volume
-    variant match the oracle like the default NVRTC-specialised kernel."""
+    """The ahead-of-time (bytecode-interpreted) kernels, the plain volume
+    variant, the opt-in bulk-copy (TMA) staging, the wide-register build and
+    the padding / unrolling switches match the oracle like the default
+    NVRTC-specialised kernel."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     if case == "vardiff":
