@@ -34,6 +34,54 @@ __device__ __forceinline__ void raise_flag(uint32_t* flags, uint32_t bit) {
   if (flags) atomicOr(flags, bit);
 }
 
+// sin(pi x) / cos(pi x) of the runtime-specialised volume fields (model.py
+// lowers sin/cos((k pi) u) to these).  Reduction r = x - rint(x) in [-1/2, 1/2]
+// is exact; sin(pi r) is the odd Taylor polynomial to r^23 (truncation below
+// 1e-18; <= 1.5 ulp against mpmath over [-3, 3]); cos(pi r) = sin(pi (1/2 - |r|))
+// (exact argument, so cospi(1/2) = 0); the sign is the parity of rint(x).
+// About 17 instructions against ~35 for CUDA's sinpi: the cfg5 source term
+// sin(pi x) sin(pi y) was 10% of the element kernel's instructions (r02 ncu).
+// PDG_FAST_SINPI=0 selects CUDA's sinpi / cospi.
+#ifndef PDG_FAST_SINPI
+#define PDG_FAST_SINPI 1
+#endif
+__device__ __forceinline__ double sinpi_reduced(double r) {
+  const double s = r * r;
+  double p = -1.0518471716932065e-11;
+  p = fma(p, s, 5.392664662608129e-10);
+  p = fma(p, s, -2.2948428997269873e-08);
+  p = fma(p, s, 7.952054001475513e-07);
+  p = fma(p, s, -2.1915353447830217e-05);
+  p = fma(p, s, 0.00046630280576761255);
+  p = fma(p, s, -0.0073704309457143504);
+  p = fma(p, s, 0.08214588661112823);
+  p = fma(p, s, -0.5992645293207921);
+  p = fma(p, s, 2.5501640398773455);
+  p = fma(p, s, -5.16771278004997);
+  p = fma(p, s, 3.141592653589793);
+  return r * p;
+}
+__device__ __forceinline__ double pdg_sinpi(double x) {
+#if PDG_FAST_SINPI
+  const double q = rint(x);
+  const double v = sinpi_reduced(x - q);  // inf / nan -> nan
+  const long long qi = fabs(q) < 9.0e18 ? (long long)q : 0;  // beyond 2^53 every double is even
+  return (qi & 1) ? -v : v;
+#else
+  return sinpi(x);
+#endif
+}
+__device__ __forceinline__ double pdg_cospi(double x) {
+#if PDG_FAST_SINPI
+  const double q = rint(x);
+  const double v = sinpi_reduced(0.5 - fabs(x - q));
+  const long long qi = fabs(q) < 9.0e18 ? (long long)q : 0;
+  return (qi & 1) ? -v : v;
+#else
+  return cospi(x);
+#endif
+}
+
 // Evaluate one compiled scalar field at x (stack machine; host guarantees
 // the depth fits PDG_MAX_STACK).
 static __device__ __noinline__ double eval_prog_slow(const pdg_coeffs& C, const pdg_prog p,

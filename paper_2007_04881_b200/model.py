@@ -550,7 +550,7 @@ _COP = {OP_ADD: "+", OP_SUB: "-", OP_MUL: "*", OP_DIV: "/"}
 def cuda_expr(e: Expr, sinpi: bool = True) -> str:
     """C expression with the same operation order as the numpy evaluation.
 
-    ``sinpi``: sin/cos of (k*pi)*u are emitted as sinpi/cospi(k*u) -- the
+    ``sinpi``: sin/cos of (k*pi)*u are emitted as pdg_sinpi/pdg_cospi(k*u) -- the
     same value up to the rounding of k*pi*u (<= 1 ulp of the argument),
     without the pi/2 argument reduction of sin/cos.  Off = the reference's
     own sin(fl(k*pi*u)), bit-for-bit in the argument: needed where data is
@@ -570,7 +570,7 @@ def cuda_expr(e: Expr, sinpi: bool = True) -> str:
             if c.op == OP_CONST:
                 k = _pi_multiple(float(c.value))
                 if k is not None:
-                    fn = "sinpi" if e.op == OP_SIN else "cospi"
+                    fn = "pdg_sinpi" if e.op == OP_SIN else "pdg_cospi"  # sipg_device.cuh
                     arg = rec(u) if k == 1 else f"({float(k)!r} * {rec(u)})"
                     return f"{fn}({arg})"
     if e.op in _COP:
