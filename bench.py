@@ -434,10 +434,12 @@ def run_ours(args, w, rank, world, local_rank):
                 and np.array_equal(mat_h.values[::st], plan.values[::st].cpu().numpy())
                 and np.array_equal(mat_h.col_idx[::st], plan.col_idx[::st].cpu().numpy()))
             e2e_host["how"] = ("D2H into page-locked host CSR arrays (pdg_host_alloc, kept across steps, "
-                               "HostIO.result()); col_idx crosses the link once per element (each element's "
-                               "first row, pdg_pack_block_cols) and host threads write it into every row "
-                               "(pdg_expand_block_cols) while the values transfer; checked against the device CSR "
-                               "after the "
+                               "HostIO.result()); "
+                               + ("col_idx crosses the link once per element (each element's first row, "
+                                  "pdg_pack_block_cols) and host threads write it into every row "
+                                  "(pdg_expand_block_cols) while the values transfer; " if io.packed_cols else
+                                  "every row of col_idx over the link (CSR below the packing threshold); ")
+                               + "checked against the device CSR after the "
                                f"timed region (row_ptr, rhs whole; values, col_idx every {st}th entry)")
             del mat_h, rhs_hh
         else:

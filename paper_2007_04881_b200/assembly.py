@@ -894,6 +894,11 @@ class SipgPlan:
         return out
 
 
+# below this col_idx size the per-element packing (a kernel, an event wait and
+# host threads) costs more than the bytes it saves (r02h: cfg1 e2e 5.5 -> 1.8 M el/s)
+_COMPACT_MIN_BYTES = 1 << 28
+
+
 class HostIO:
     """Host buffers for end-to-end runs of a plan (a caller that keeps its
     result arrays across assemblies).
@@ -904,15 +909,15 @@ class HostIO:
     page-locked host arrays (``pdg_host_alloc``: the copies are DMA at the
     link rate -- on the box 51 GB/s, against 47 GB/s into registered pageable
     arrays, tools/register_probe.py), and ``result()`` returns them as a host
-    ``CSRMatrix`` + RHS.  With ``compact_cols`` (default) col_idx crosses the
-    link once per element -- every row of an element's block row has the same
+    ``CSRMatrix`` + RHS.  With ``compact_cols`` (default: when col_idx is at
+    least 256 MB) col_idx crosses the link once per element -- every row of an element's block row has the same
     columns -- and host threads expand it into every row while the values
     are in flight (cfg5: 54 instead of 102 GB per step).  When the allocation fails, or with
     ``retain=False``, the bytes go through a pinned ring of ``chunk_bytes``
     and nothing is retained (``retained`` says which)."""
 
     def __init__(self, plan: "SipgPlan", chunk_bytes: int = 1 << 30, retain: bool = True,
-                 compact_cols: bool = True):
+                 compact_cols: Optional[bool] = None):
         torch = _torch()
         self.plan = plan
         self.inputs = {}
@@ -929,7 +934,7 @@ class HostIO:
             try:
                 for t in outs:
                     self.host.append(_pinned_empty(t))
-                if compact_cols:
+                if compact_cols or (compact_cols is None and int(plan.col_idx.numel()) * 8 >= _COMPACT_MIN_BYTES):
                     self._setup_compact()
             except RuntimeError:  # out of page-lockable memory: fall back to the ring
                 self.close()
@@ -950,12 +955,18 @@ class HostIO:
         self._packed = torch.empty(max(total, 1), dtype=torch.int64, device=p.values.device)
         self._packed_h = _pinned_empty(self._packed)
         self._event = torch.cuda.Event()
-        self._threads = max(1, min(16, os.cpu_count() or 1))
+        # a host thread per 16 MB of col_idx written, at most 16
+        self._threads = max(1, min(16, os.cpu_count() or 1, int(p.col_idx.numel()) * 8 >> 24))
         self.d2h_bytes = sum(int(t.numel() * t.element_size()) for t in (p.row_ptr, p.values, p.rhs)) + 8 * total
 
     @property
     def retained(self) -> bool:
         return bool(self.host)
+
+    @property
+    def packed_cols(self) -> bool:
+        """col_idx crosses the link once per element (expanded on the host)."""
+        return bool(self.host) and getattr(self, "_packed_h", None) is not None
 
     def upload(self):
         torch = _torch()
@@ -967,7 +978,7 @@ class HostIO:
         torch = _torch()
         p = self.plan
         outs = (p.row_ptr, p.col_idx, p.values, p.rhs)
-        if self.host and getattr(self, "_packed_h", None) is not None:
+        if self.packed_cols:
             return self._download_compact()
         with torch.cuda.stream(p.stream):
             if self.host:

@@ -335,7 +335,7 @@ def test_hostio_retained_host_csr_matches_assembly():
     specs = build_basis(pm, 3)
     m, rhs, _, _ = assemble_approach2(pm, coeffs, specs)
     plan = SipgPlan(pm, coeffs, specs)
-    io = HostIO(plan)
+    io = HostIO(plan, compact_cols=True)  # (auto mode packs only CSRs of >= 256 MB)
     assert io.retained
     for _ in range(2):
         io.upload()
