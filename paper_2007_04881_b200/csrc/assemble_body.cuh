@@ -484,12 +484,13 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       const int r0 = R.vol_offset[order], nq = R.vol_count[order];
       const int64_t s0 = m.elem_ptr[e];
       const int Q = (int)(m.elem_ptr[e + 1] - s0) * nq;
+      const float rnq = 1.0f / (float)nq;
       for (int base = 0; base < Q; base += kv) {
         const int nvalid = min(kv, Q - base);
         if (lane < kv) {
           const int gq = base + min(lane, nvalid - 1);
           const double valid = lane < nvalid ? 1.0 : 0.0;
-          const int ls = gq / nq;
+          const int ls = small_div(gq, nq, rnq);
           const int kq = gq - ls * nq;
           const double* xi = RV.pts + (r0 + kq) * 3;
           double x[3] = {0.0, 0.0, 0.0};
@@ -918,10 +919,11 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           }
           const bool first_face = STAGE_BOX && f == rc[qi].fa;
           const int Pf = nrows * nq;
+          const float rnq = 1.0f / (float)nq;
           for (int base = 0; base < Pf; base += KF) {
             const int nvalid = min(KF, Pf - base);
             const int gq = base + min(slot, nvalid - 1);
-            const int lr = gq / nq;
+            const int lr = small_div(gq, nq, rnq);
             // the first sub-facet frame of the interface is staged (ffr)
             const double* frp = (first_face && lr == 0) ? ffr + qi * W::FF : a.fframe + (row0 + lr) * W::FF;
             tab_slot(nrm, frp, r0, gq - lr * nq, slot < nvalid ? 1.0 : 0.0, sig, side ? -1.0 : 1.0,
@@ -956,6 +958,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
       for (int i = 0; i < DIM; ++i) nrm[i] = m.face_normal[(int64_t)f * DIM + i];
       const int64_t row0 = m.face_ptr[f];
       const int Pf = (int)(m.face_ptr[f + 1] - row0) * nq;
+      const float rnq = 1.0f / (float)nq;
       const int slot = lane & (KF - 1);
       const bool mine = lane < KF;
       const bool use_f = tag == PDG_TAG_DIRICHLET && grad_terms;
@@ -964,7 +967,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
         {
           const int gq = base + min(slot, nvalid - 1);
           const double valid = (slot < nvalid && mine) ? 1.0 : 0.0;
-          const int lr = gq / nq;
+          const int lr = small_div(gq, nq, rnq);
           const int kq = gq - lr * nq;
           const double* xi = RV.pts + (r0 + kq) * 3;
           double x[3] = {0.0, 0.0, 0.0};
