@@ -49,11 +49,13 @@ __device__ __forceinline__ void elem_abar_body(const pdg_mesh& m, const pdg_basi
     const int order = 2 * B.degree[e] + prm.quad_increment;
     const int r0 = R.vol_offset[order], nq = R.vol_count[order];
     const int64_t s0 = m.elem_ptr[e];
-    const int64_t Q = (m.elem_ptr[e + 1] - s0) * nq;
+    const int Q = (int)(m.elem_ptr[e + 1] - s0) * nq;
+    const float rnq = 1.0f / (float)nq;
     double best = -PDG_INF;
-    for (int64_t g = lane; g < Q; g += 32) {
-      const int s = m.elem_simplices[s0 + g / nq];
-      const int k = (int)(g % nq);
+    for (int g = lane; g < Q; g += 32) {
+      const int ls = small_div(g, nq, rnq);
+      const int s = m.elem_simplices[s0 + ls];
+      const int k = g - ls * nq;
       double v0[3], E[3][3];
       simplex_frame<DIM>(m, s, v0, E, flags);
       double x[3] = {0, 0, 0};

@@ -409,9 +409,9 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         {
           const int gq = base + min(lane, nvalid - 1);
           const double valid = lane < nvalid ? 1.0 : 0.0;
-          const int ls = gq / nq;
+          const int ls = small_div(gq, nq, 1.0f / (float)nq);
           const int rem = gq - ls * nq;
-          const int is = rem / nqt, it = rem - is * nqt;
+          const int is = small_div(rem, nqt, 1.0f / (float)nqt), it = rem - is * nqt;
           const double* fr = a.sframe + (s0 + ls) * FW;
           double x[4];
           const double det = frame_point<S, S>(fr, R.points + (r0s + is) * 3, x);
@@ -626,7 +626,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
             const int nqf = nqe * nqt;
             const double valid = ls < nqf ? 1.0 : 0.0;
             const int gq = min(ls, nqf - 1);
-            const int ie = gq / nqt, it = gq - ie * nqt;
+            const int ie = small_div(gq, nqt, 1.0f / (float)nqt), it = gq - ie * nqt;
             const int side = nb_info[q] & 1;
             const double sgn = side ? -1.0 : 1.0;
             const bool down = CF::has_adv() && (nb_info[q] & 2) != 0;
@@ -696,9 +696,9 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
           {
             const int gq = base + min(lane, nvalid - 1);
             const double valid = lane < nvalid ? 1.0 : 0.0;
-            const int lr = gq / nqf;
+            const int lr = small_div(gq, nqf, 1.0f / (float)nqf);
             const int rem = gq - lr * nqf;
-            const int ie = rem / nqt, it = rem - ie * nqt;
+            const int ie = small_div(rem, nqt, 1.0f / (float)nqt), it = rem - ie * nqt;
             double x[4];
             const double jac = frame_point<S, S - 1>(a.fframe + (row0 + lr) * FW, R.points + (r0e + ie) * 3, x);
             x[S] = t0 + tau * TR_.points[(r0t + it) * 3];
@@ -759,9 +759,9 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         {
           const int gq = base + min(lane, nvalid - 1);
           const double valid = lane < nvalid ? 1.0 : 0.0;
-          const int lr = gq / nqf;
+          const int lr = small_div(gq, nqf, 1.0f / (float)nqf);
           const int rem = gq - lr * nqf;
-          const int ie = rem / nqt, it = rem - ie * nqt;
+          const int ie = small_div(rem, nqt, 1.0f / (float)nqt), it = rem - ie * nqt;
           double x[4];
           const double jac = frame_point<S, S - 1>(a.fframe + (row0 + lr) * FW, R.points + (r0e + ie) * 3, x);
           x[S] = t0 + tau * TR_.points[(r0t + it) * 3];
@@ -823,7 +823,7 @@ __device__ __forceinline__ void slab_body(const SlabArgs& a, const CF& cf) {
         {
           const int gq = base + min(lane, nvalid - 1);
           const double valid = lane < nvalid ? 1.0 : 0.0;
-          const int ls = gq / nqs;
+          const int ls = small_div(gq, nqs, 1.0f / (float)nqs);
           const int is = gq - ls * nqs;
           double x[4];
           const double det = frame_point<S, S>(a.sframe + (s0 + ls) * FW, R.points + (r0s + is) * 3, x);
