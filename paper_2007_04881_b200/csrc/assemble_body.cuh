@@ -82,6 +82,11 @@ namespace pdg {
 #define PDG_PAD_ZERO -1
 #endif
 
+// constant isotropic diffusion: the volume's sqrt-weight scaling folded into the
+// Legendre recurrence start (1), or applied to the tabulated factors (0)
+#ifndef PDG_FOLD_SW
+#define PDG_FOLD_SW 1
+#endif
 // phase timers (diagnostics: one warp prints its clock64 split at exit)
 #ifndef PDG_TIMERS
 #define PDG_TIMERS 0
@@ -497,15 +502,22 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           const double* fr = fr_smem ? sfr + ls * W::SF : a.sframe + (s0 + ls) * W::SF;
           const double det = frame_point<DIM, DIM>(fr, xi, x);
           const double w = RV.w[r0 + kq] * det * valid;
+          // constant isotropic a without advection / reaction rows: the sqrt
+          // weight enters through the recurrence start of the dim-0 factors (one
+          // product instead of 2(P+1)), and the RHS uses w f phi = (f sw / a) (sw phi)
+          const bool fold = PDG_FOLD_SW && nG && sqrtw && !has_vr && cf.a_const();
+          double av = 1.0, sw = 0.0;
+          if (nG && sqrtw) {
+            av = cf.a_iso(x);
+            if (av < 0.0) raise_flag(a.flags, PDG_FLAG_NEG_DIFFUSION);
+            sw = RV.sw[r0 + kq] * fr[DIM + DIM * DIM + 1] * sqrt(fmax(av, 0.0)) * valid;
+          }
           Tab<DIM, P> tb;
-          tb.load(bx, x);
+          tb.load(bx, x, fold ? sw : 1.0);
           double* col = buf + lane;
           if (nG && sqrtw) {
-            const double av = cf.a_iso(x);
-            if (av < 0.0) raise_flag(a.flags, PDG_FLAG_NEG_DIFFUSION);
-            const double sw = RV.sw[r0 + kq] * fr[DIM + DIM * DIM + 1] * sqrt(fmax(av, 0.0)) * valid;
             Tab<DIM, P> ts = tb;
-            ts.scale(sw);
+            if (!fold) ts.scale(sw);
 #pragma unroll
             for (int c = 0; c < DIM; ++c)
 #pragma unroll
@@ -558,7 +570,7 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
             }
           }
           if (cf.has_src()) {
-            const double wf = w * cf.f(x);
+            const double wf = fold ? cf.f(x) * (sw * (1.0 / av)) : w * cf.f(x);
             // phi_f = X_a Y_b (Z_c): fold w f into the x-factors once (P+1 products
             // instead of one per function)
             constexpr MultiIdx<DIM, P> mi{};

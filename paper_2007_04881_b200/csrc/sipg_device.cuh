@@ -243,9 +243,11 @@ struct Tab {
   static constexpr int NB = binom(P + DIM, DIM);
   double v1[DIM][P + 1], d1[DIM][P + 1];
 
-  __device__ __forceinline__ void load(const BoxConst<DIM>& b, const double* x) {
+  // s0 scales every function (the dim-0 factors, through the recurrence's start)
+  __device__ __forceinline__ void load(const BoxConst<DIM>& b, const double* x, double s0 = 1.0) {
 #pragma unroll
-    for (int i = 0; i < DIM; ++i) legendre_1d<P>((x[i] - b.c[i]) * b.ih[i], b.rs[i], b.ih[i], v1[i], d1[i]);
+    for (int i = 0; i < DIM; ++i)
+      legendre_1d<P>((x[i] - b.c[i]) * b.ih[i], i == 0 ? b.rs[i] * s0 : b.rs[i], b.ih[i], v1[i], d1[i]);
   }
   // multiply every basis function (and gradient) by s: scale the dim-0 factors
   __device__ __forceinline__ void scale(double s) {
