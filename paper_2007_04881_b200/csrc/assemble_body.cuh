@@ -87,6 +87,9 @@ namespace pdg {
 #ifndef PDG_FOLD_SW
 #define PDG_FOLD_SW 1
 #endif
+#ifndef PDG_COL_PTR
+#define PDG_COL_PTR 1
+#endif
 // phase timers (diagnostics: one warp prints its clock64 split at exit)
 #ifndef PDG_TIMERS
 #define PDG_TIMERS 0
@@ -849,8 +852,14 @@ __device__ __forceinline__ void assemble_body(const KArgs& a, const CF& cf) {
           while (q + 1 < nw && rc[q + 1].col <= p) ++q;
           const int64_t cv = rc[q].dof + (p - rc[q].col);
           int64_t* dst = pat.col_idx + voff + p;
+#if PDG_COL_PTR
+          // running pointer: one 64-bit add per row instead of a wide multiply-add
+#pragma unroll 4
+          for (int r = 0; r < ne; ++r, dst += Lrow) st_out<int64_t>(dst, cv);
+#else
 #pragma unroll 4
           for (int r = 0; r < ne; ++r) st_out<int64_t>(dst + (int64_t)r * Lrow, cv);
+#endif
         }
       }
       PDG_T(4)
